@@ -1,0 +1,421 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Every test cites the passage (PAPER.md line numbers, "P:n") whose number,
+closed form or property it checks.  None of them re-types the oracle's own
+formula: the expected values come from the paper's tables (tests/golden/),
+closed-form symbols printed in the paper, Taylor-order arguments, brute-force
+loops on tiny grids, or textbook identities.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import lfa
+from oracle.cycle import cycle, smooth, vcycle
+from oracle.fgmres import convergence_factor, fgmres_solve
+from oracle.hierarchy import Options, build_hierarchy, coarse_solve, operator_complexity, stencil_radius
+from oracle.intergrid import prolongation, restriction
+from oracle.operators import (COMPACT4, FD2, L_stencil, M_stencil, fine_operator, node_coords,
+                              sigma_fields, stencil_matrix)
+from oracle.vanka import patch_counts, patch_matrices, patches, vanka_operator
+from paper_2511_16808_b200 import media
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_tables.json")))
+
+
+def plane_wave(nodes, theta):
+    c = node_coords(nodes)
+    return np.exp(1j * sum(t * ci for t, ci in zip(theta, c)))
+
+
+def interior_mask(nodes, margin):
+    c = node_coords(nodes)
+    m = np.ones(int(np.prod(nodes)), bool)
+    for a, n in enumerate(nodes):
+        m &= (c[a] >= margin) & (c[a] < n - margin)
+    return m
+
+
+# ----------------------------------------------------------------- discretisation
+@pytest.mark.parametrize("theta", [(0.3, -1.1), (2.0, 0.7), (np.pi, 0.0)])
+def test_stencil_symbol_2d(theta):
+    """Eq. 4.2: the compact 9-point operator acts on a plane wave as
+    a + 2b cos t1 + 2b cos t2 + 4c cos t1 cos t2 at every interior node."""
+    h, sigma = 1 / 32, 900.0 - 120.0j
+    nodes = (33, 33)
+    H = fine_operator(nodes, h, np.full(33 * 33, sigma))
+    v = plane_wave(nodes, theta)
+    a = 10 / (3 * h * h) - 2 * sigma / 3
+    b = -2 / (3 * h * h) - sigma / 12
+    c = -1 / (6 * h * h)
+    sym = a + 2 * b * np.cos(theta[0]) + 2 * b * np.cos(theta[1]) + 4 * c * np.cos(theta[0]) * np.cos(theta[1])
+    m = interior_mask(nodes, 1)
+    np.testing.assert_allclose((H @ v)[m], sym * v[m], rtol=1e-12)
+
+
+@pytest.mark.parametrize("theta", [(0.3, -1.1, 0.5), (2.0, 0.7, -2.9)])
+def test_stencil_symbol_3d(theta):
+    """Eq. 2.3 on a plane wave: symbol derived by hand from the
+    printed planes: 4/h^2 - sigma/2 - (2/(3h^2) + sigma/6) sum cos
+    - (2/(3h^2)) sum_{k<l} cos cos."""
+    h, sigma = 1 / 16, 400.0 - 50.0j
+    nodes = (17, 17, 17)
+    H = fine_operator(nodes, h, np.full(17 ** 3, sigma))
+    v = plane_wave(nodes, theta)
+    cs = np.cos(theta)
+    sym = 4 / h ** 2 - sigma / 2 - (2 / (3 * h * h) + sigma / 6) * cs.sum() \
+        - (2 / (3 * h * h)) * (cs[0] * cs[1] + cs[0] * cs[2] + cs[1] * cs[2])
+    m = interior_mask(nodes, 1)
+    np.testing.assert_allclose((H @ v)[m], sym * v[m], rtol=1e-12)
+
+
+def test_stencil_support_sizes():
+    """9-point (2D) and 19-point (3D) compact stencils; 5/7-point FD2."""
+    assert len(L_stencil(2, 1.0)[0]) == 9
+    assert len(L_stencil(3, 1.0)[0]) == 19
+    assert len(L_stencil(2, 1.0, FD2)[0]) == 5 and len(L_stencil(3, 1.0, FD2)[0]) == 7
+    assert np.isclose(sum(L_stencil(3, 1.0)[1]), 0) and np.isclose(sum(L_stencil(2, 1.0)[1]), 0)
+    assert np.isclose(sum(M_stencil(2)[1]), 1) and np.isclose(sum(M_stencil(3)[1]), 1)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_mehrstellen_fourth_order(dim):
+    """Compact scheme ([singer1998high]): L u - M(-Delta u) = O(h^4)
+    while L u + Delta u = O(h^2): error ratios ~16 vs ~4 per halving."""
+    errs4, errs2 = [], []
+    for n in ([8, 16, 32] if dim == 3 else [16, 32, 64]):
+        h = 1.0 / n
+        nodes = (n + 1,) * dim
+        c = [ci * h for ci in node_coords(nodes)]
+        k = np.array([1.0, 2.0, 1.5][:dim]) * np.pi
+        u = np.prod([np.sin(k[a] * c[a]) for a in range(dim)], axis=0)
+        lap = -np.sum(k ** 2) * u
+        L = stencil_matrix(nodes, *L_stencil(dim, h))
+        M = stencil_matrix(nodes, *M_stencil(dim))
+        m = interior_mask(nodes, 1)
+        errs4.append(np.abs((L @ u - M @ (-lap))[m]).max())
+        errs2.append(np.abs((L @ u + lap)[m]).max())
+    r4 = errs4[0] / errs4[1], errs4[1] / errs4[2]
+    r2 = errs2[0] / errs2[1], errs2[1] / errs2[2]
+    assert min(r4) > 12 and max(r2) < 5
+
+
+def test_shift_reading():
+    """Eq. 2.6 with readings A1/A2: H_s = H + i alpha omega^2 kappa^2 M (the shift
+    adds attenuation).  Checked on an explicit 3-node example."""
+    kappa = np.array([1.0, 0.5, 2.0])
+    gamma = np.array([0.0, 3.0, 1.0])
+    omega, alpha = 10.0, 0.3
+    s, ss = sigma_fields(kappa, gamma, omega, alpha)
+    # Eq. 1.1: sigma = omega^2 kappa^2 (1 - i gamma/omega)
+    np.testing.assert_allclose(s, [100.0, 25.0 * (1 - 0.3j), 400.0 * (1 - 0.1j)])
+    np.testing.assert_allclose(ss - s, -1j * alpha * omega ** 2 * kappa ** 2)
+    assert np.all(ss.imag < s.imag)   # more attenuation (same sign as gamma)
+
+
+# ----------------------------------------------------------------- intergrid
+@pytest.mark.parametrize("kind", ["lin", "cub"])
+def test_restriction_symbol(kind):
+    """Intergrid symbols P:652-660 at interior coarse nodes."""
+    nodes = (33, 33)
+    R = restriction(nodes, kind)
+    theta = (0.7, -1.3)
+    v = plane_wave(nodes, theta)
+    cn = (17, 17)
+    cc = node_coords(cn)
+    fine_of_coarse = 2 * cc[0] + 33 * 2 * cc[1]
+    m = interior_mask(cn, 2)
+    sym = lfa.restriction_symbol(kind, *theta)
+    if kind == "lin":
+        assert np.isclose(sym, 0.25 * (1 + np.cos(0.7)) * (1 + np.cos(-1.3)))
+    np.testing.assert_allclose((R @ v)[m], sym * v[fine_of_coarse][m], rtol=1e-12)
+
+
+def test_prolongation_weights_and_polynomials():
+    """P = 4 R^T: bicubic P is cubic-B-spline subdivision (3/4, 1/8, 1/8 at
+    coincident nodes, 1/2, 1/2 in between); bilinear P is linear interpolation;
+    both reproduce linear functions at interior fine nodes."""
+    P1 = prolongation((17,), "cub").toarray()
+    np.testing.assert_allclose(P1[8, 3:6], [1 / 8, 3 / 4, 1 / 8])
+    np.testing.assert_allclose(P1[9, 4:6], [1 / 2, 1 / 2])
+    Pl = prolongation((17,), "lin").toarray()
+    np.testing.assert_allclose(Pl[8, 4], 1.0)
+    np.testing.assert_allclose(Pl[9, 4:6], [1 / 2, 1 / 2])
+    for kind in ("lin", "cub"):
+        P = prolongation((33, 17), kind)
+        cc = node_coords((17, 9))
+        e = 3.0 * cc[0] - 2.0 * cc[1] + 1.0
+        fc = node_coords((33, 17))
+        target = 3.0 * fc[0] / 2 - 2.0 * fc[1] / 2 + 1.0
+        m = interior_mask((33, 17), 2)
+        np.testing.assert_allclose((P @ e)[m], target[m], rtol=1e-13, atol=1e-12)
+    # 3D: 8 R^T -- a constant coarse function maps to a constant
+    P3 = prolongation((9, 9, 9), "cub")
+    m = interior_mask((9, 9, 9), 2)
+    np.testing.assert_allclose((P3 @ np.ones(125))[m], 1.0)
+
+
+# ----------------------------------------------------------------- Galerkin
+@pytest.mark.slow
+def test_table_3_1_operator_complexity():
+    """Table 3.1: operator complexity of 2..5-level Galerkin
+    hierarchies for a 64^3-cell grid (Eq. 3.7)."""
+    g = GOLD["table_3_1_operator_complexity_64cube"]
+    p = media.homogeneous_problem(3, 64, sponge=20, gamma_max_over_omega=1.0)
+    for scheme, key in (("cubic", "tricubic"), ("levdep", "levdep"), ("linear", "trilinear")):
+        opts = Options(dim=3, cells=p.cells, h=p.h, levels=5, intergrid=scheme, smoother="element")
+        hier = build_hierarchy(opts, p.kappa, p.omega, p.gamma, 0.0, build_smoothers=False)
+        nnz = [A.count_nonzero() for A in hier.A]
+        got = [sum(nnz[:k]) / nnz[0] for k in range(2, 6)]
+        for lv, (a, b) in enumerate(zip(got, g[key])):
+            tol = 0.004 if (key == "trilinear" and lv == 2) else 6e-4
+            assert abs(a - b) < tol, (key, lv + 2, a, b)
+        radii = [stencil_radius(A, n) for A, n in zip(hier.A, hier.nodes)]
+        # P:364-365 / P:400: lin stays 3^3, cubic grows to 7^3, lev-dep/mixed <= 5^3
+        assert max(radii) == {"tricubic": 3, "levdep": 2, "trilinear": 1}[key]
+
+
+def test_galerkin_is_R_A_P_levdep_2d():
+    """Coarse operator = R_l A_l P_l with the level-dependent pair of
+    Eqs. 3.3-3.4: brute-force triple sum over the dense matrices on a tiny grid."""
+    p = media.homogeneous_problem(2, 16, sponge=4)
+    opts = Options(dim=2, cells=p.cells, h=p.h, levels=3)
+    hier = build_hierarchy(opts, p.kappa, p.omega, p.gamma, 0.2, build_smoothers=False)
+    A1 = hier.A[0].toarray()
+    R1 = np.kron(*(restriction((17,), "cub").toarray(),) * 2)
+    P1 = 4 * np.kron(*(restriction((17,), "cub").toarray(),) * 2).T
+    A2 = np.einsum("ij,jk,kl->il", R1, A1, P1)
+    np.testing.assert_allclose(hier.A[1].toarray(), A2, rtol=1e-12, atol=1e-9 * np.abs(A2).max())
+    R2 = np.kron(*(restriction((9,), "lin").toarray(),) * 2)
+    P2 = 4 * np.kron(*(restriction((9,), "cub").toarray(),) * 2).T
+    A3 = np.einsum("ij,jk,kl->il", R2, A2, P2)
+    np.testing.assert_allclose(hier.A[2].toarray(), A3, rtol=1e-12, atol=1e-9 * np.abs(A3).max())
+
+
+# ----------------------------------------------------------------- Vanka
+def test_boundary_patch_sizes_and_weights():
+    """clipped boundary patches -- plus: 3-point corners, 4-point
+    edges; RB: 2-point corners, 3-point edges; weights 1/count, equal weighting
+    1/N in the interior; element patches are not clipped."""
+    nodes = (9, 9)
+    sizes = {k: dict(patches(nodes, k)) for k in ("plus", "rb", "element")}
+    assert sorted(sizes["plus"]) == [3, 4, 5] and len(sizes["plus"][3]) == 4
+    assert len(sizes["plus"][4]) == 4 * 7
+    assert sorted(sizes["rb"]) == [2, 3, 5] and len(sizes["rb"][2]) == 4 and len(sizes["rb"][3]) == 28
+    assert list(sizes["element"]) == [4] and len(sizes["element"][4]) == 64
+    cnt = patch_counts(nodes, "rb").reshape(9, 9)
+    assert cnt[4, 4] == 5 and cnt[0, 4] == 3 and cnt[0, 0] == 2
+    cnt = patch_counts(nodes, "element").reshape(9, 9)
+    assert cnt[4, 4] == 4 and cnt[0, 4] == 2 and cnt[0, 0] == 1
+    c3 = patch_counts((5, 5, 5), "element").reshape(5, 5, 5)
+    assert c3[2, 2, 2] == 8 and c3[0, 2, 2] == 4 and c3[0, 0, 2] == 2 and c3[0, 0, 0] == 1
+
+
+@pytest.mark.parametrize("kind", ["rb", "plus", "element", "jacobi"])
+def test_partition_of_unity(kind):
+    """sum_i V_i^T W_i V_i = I (weights are 1/count per node)."""
+    nodes = (9, 7)
+    N = 63
+    cnt = patch_counts(nodes, kind)
+    acc = np.zeros(N)
+    for _, P in patches(nodes, kind):
+        np.add.at(acc, P.ravel(), 1.0 / cnt[P.ravel()])
+    np.testing.assert_allclose(acc, 1.0)
+
+
+def test_jacobi_is_damped_jacobi():
+    """1x1 Vanka == damped point Jacobi: B = diag(A)^{-1}."""
+    p = media.homogeneous_problem(2, 8, sponge=2)
+    s, ss = sigma_fields(p.kappa, p.gamma, p.omega, 0.3)
+    A = fine_operator(p.nodes, p.h, ss)
+    B, _ = vanka_operator(A, p.nodes, "jacobi")
+    np.testing.assert_allclose(B.toarray(), np.diag(1.0 / A.diagonal()))
+
+
+@pytest.mark.parametrize("kind,dim", [("rb", 2), ("plus", 2), ("element", 2), ("element", 3)])
+def test_vanka_brute_force_loop(kind, dim):
+    """Eq. 3.8 / Eq. 3.7 update by a literal per-patch loop:
+    solve H_i e_i = V_i r, u += w W_i e_i -- versus the assembled smoother."""
+    p = media.homogeneous_problem(dim, 8 if dim == 2 else 4, sponge=2)
+    kappa = p.kappa * (1 + 0.2 * np.random.default_rng(0).random(p.kappa.shape))
+    s, ss = sigma_fields(kappa, p.gamma, p.omega, 0.3)
+    A = fine_operator(p.nodes, p.h, ss)
+    f = media.random_complex(p.n, 1)
+    u = media.random_complex(p.n, 2)
+    w = 0.7
+    B, cnt = vanka_operator(A, p.nodes, kind)
+    ref = u + w * (B @ (f - A @ u))
+    r = f - A @ u
+    Ad = A.toarray()
+    out = u.copy()
+    for _, P in patches(p.nodes, kind):
+        for X in P:
+            e = np.linalg.solve(Ad[np.ix_(X, X)], r[X])
+            out[X] += w * e / cnt[X]
+    np.testing.assert_allclose(out, ref, rtol=1e-11)
+
+
+@pytest.mark.parametrize("kind", ["jacobi", "element", "plus", "rb"])
+def test_vanka_matches_lfa_symbol(kind):
+    """Interior action of the assembled additive-Vanka smoother on a plane wave
+    equals the paper's smoother symbol Eq. 4.1 with the patch matrices of
+    Eqs. 4.3-4.7, constant coefficients, gamma = 0."""
+    n = 24
+    h = 1.0 / n
+    nodes = (n + 1, n + 1)
+    omega = 2 * np.pi / (10 * h)
+    sigma = omega ** 2 * (1 - 0.2j)
+    A = fine_operator(nodes, h, np.full(int(np.prod(nodes)), sigma))
+    B, _ = vanka_operator(A, nodes, kind)
+    w = 0.8
+    for theta in [(0.4, 1.7), (2.5, -0.3)]:
+        v = plane_wave(nodes, theta)
+        Sv = v - w * (B @ (A @ v))
+        m = interior_mask(nodes, 3)
+        sym = lfa.smoother_symbol(kind, theta[0], theta[1], sigma, h, w)
+        np.testing.assert_allclose(Sv[m], sym * v[m], rtol=1e-10)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind", ["jacobi", "element", "plus", "rb"])
+def test_lfa_two_grid_argmin_is_table_5_1(kind):
+    """Table 5.1 fine-level damping = argmin_w rho_loc (Fig. 5.1):
+    256^2, 10 ppw, alpha = 0, bicubic 2-grid V(1,1)."""
+    h = 1.0 / 256
+    sigma = (2 * np.pi / (10 * h)) ** 2
+    expect = GOLD["table_5_1_damping"]["fine_2d"][kind]
+    fine = np.round(np.arange(expect - 0.04, expect + 0.0401, 0.01), 2)
+    wbest, rbest = lfa.argmin_damping(lambda w: lfa.rho_loc(kind, sigma, h, w, n=256), fine)
+    assert abs(wbest - expect) < 1e-9, (kind, wbest)
+    coarse = np.arange(0.5, 1.201, 0.1)
+    assert all(lfa.rho_loc(kind, sigma, h, w, n=256) >= rbest - 1e-12 for w in coarse)
+
+
+# ----------------------------------------------------------------- cycle / Krylov
+def test_two_grid_error_propagation_eq_2_4():
+    """A 2-level V(1,1) cycle has error propagation S (I - P A_c^{-1} R A) S
+    (Eq. 2.4): compare on unit vectors of a 9x9 grid."""
+    p = media.homogeneous_problem(2, 8, sponge=2)
+    opts = Options(dim=2, cells=p.cells, h=p.h, levels=2)
+    hier = build_hierarchy(opts, p.kappa, p.omega, p.gamma, 0.3)
+    A = hier.A[0].toarray()
+    N = A.shape[0]
+    S = np.eye(N) - opts.damping_at(0) * hier.B[0].toarray() @ A
+    TG = S @ (np.eye(N) - hier.P[0].toarray() @ np.linalg.solve(
+        hier.A[1].toarray(), hier.R[0].toarray() @ A)) @ S
+    f = np.zeros(N, complex)
+    E = np.empty((N, N), complex)
+    for k in range(N):
+        e0 = np.zeros(N, complex)
+        e0[k] = 1.0
+        # error propagation: u_exact = 0 for f = 0, so the new error is the new iterate
+        E[:, k] = cycle(hier, 0, f, e0)
+    np.testing.assert_allclose(E, TG, rtol=1e-10, atol=1e-12)
+
+
+def test_coarsest_direct_solve_residual():
+    """Coarsest direct solve: relative residual <= 1e-12."""
+    p = media.homogeneous_problem(2, 32, sponge=4)
+    hier = build_hierarchy(Options(dim=2, cells=p.cells, h=p.h, levels=3), p.kappa, p.omega, p.gamma, 0.2)
+    r = media.random_complex(hier.A[-1].shape[0], 3)
+    e = coarse_solve(hier, r)
+    assert np.linalg.norm(hier.A[-1] @ e - r) / np.linalg.norm(r) < 1e-12
+
+
+def test_fgmres_exact_preconditioner_one_iteration():
+    """Right-preconditioned FGMRES with M^{-1} = A^{-1} converges in one
+    iteration; on a dense 5x5 system it returns the direct solution."""
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((5, 5)) + 1j * rng.standard_normal((5, 5)) + 4 * np.eye(5)
+    q = rng.standard_normal(5) + 0j
+    x, info = fgmres_solve(A, q, lambda v: np.linalg.solve(A, v), restart=5, tol=1e-10)
+    assert info["iterations"] == 1
+    np.testing.assert_allclose(x, np.linalg.solve(A, q), rtol=1e-10)
+    x, info = fgmres_solve(A, q, lambda v: v, restart=5, tol=1e-12)
+    assert info["iterations"] <= 5 and info["converged"]
+    np.testing.assert_allclose(x, np.linalg.solve(A, q), rtol=1e-9)
+    h = np.array(info["history"])
+    assert np.all(np.diff(h) <= 1e-15)
+
+
+def test_convergence_factor_definition():
+    """Eq. 5.1 on a geometric sequence with a 5-iteration warm-up."""
+    hist = [1.0, 0.9, 0.5, 0.4, 0.3, 0.2] + [0.2 * 0.5 ** k for k in range(1, 6)]
+    assert np.isclose(convergence_factor(hist, 5), 0.5)
+
+
+def _solve(prob, dim, smoother, alpha, levels=4, cyc="W", restart=5, scheme="levdep"):
+    opts = Options(dim=dim, cells=prob.cells, h=prob.h, levels=levels, intergrid=scheme,
+                   smoother=smoother, cycle=cyc)
+    hier = build_hierarchy(opts, prob.kappa, prob.omega, prob.gamma, alpha)
+    x, info = fgmres_solve(hier.H, prob.q.ravel(), lambda v: vcycle(hier, v), restart=restart,
+                           tol=1e-6, maxiter=400)
+    assert info["converged"] and info["true_relres"] < 1e-6
+    return info["iterations"]
+
+
+def test_table_5_2_rb_levdep_128():
+    """Table 5.2: RB patch + level-dependent intergrid, 4-level W(1,1),
+    GMRES(5), alpha = 0.18, 128^2 cells -> 20 iterations (paper ABC: 20 cells)."""
+    p = media.homogeneous_problem(2, 128, sponge=20, gamma_max_over_omega=1.0)
+    assert _solve(p, 2, "rb", 0.18) == GOLD["table_5_2_iterations_128"]["rb_levdep"]["128"]
+
+
+@pytest.mark.slow
+def test_table_5_2_rb_levdep_256():
+    p = media.homogeneous_problem(2, 256, sponge=20, gamma_max_over_omega=1.0)
+    assert _solve(p, 2, "rb", 0.18) == GOLD["table_5_2_iterations_128"]["rb_levdep"]["256"]
+
+
+@pytest.mark.parametrize("smoother,alpha,key", [("jacobi", 0.3, "jacobi_levdep"),
+                                                ("element", 0.25, "element_levdep"),
+                                                ("plus", 0.25, "plus_levdep")])
+def test_table_5_2_other_smoothers_within_4(smoother, alpha, key):
+    """Table 5.2 other smoothers, lev-dep: within +-4 iterations
+    (boundary layer details are unstated in the paper)."""
+    p = media.homogeneous_problem(2, 128, sponge=20, gamma_max_over_omega=1.0)
+    its = _solve(p, 2, smoother, alpha)
+    assert abs(its - GOLD["table_5_2_iterations_128"][key]["128"]) <= 4
+
+
+def test_table_5_3_linear_medium():
+    """Table 5.3 linear kappa^2 model, RB lev-dep W(1,1), 128^2:
+    3-level alpha=0.1 -> 11, 4-level alpha=0.25 -> 20 (+-1)."""
+    p = media.linear_kappa2_problem(128)
+    g = GOLD["table_5_3_linear"]
+    assert abs(_solve(p, 2, "rb", 0.1, levels=3) - g["3level_alpha0.1"]["128"]) <= 1
+    assert abs(_solve(p, 2, "rb", 0.25, levels=4) - g["4level_alpha0.25"]["128"]) <= 1
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("smoother,alpha,key", [("element", 0.4, "element_alpha0.4"),
+                                                ("jacobi", 0.5, "jacobi_alpha0.5")])
+def test_table_5_4_3d_48(smoother, alpha, key):
+    """Table 5.4: 3D homogeneous 48^3, 4-level W(1,1), GMRES(5)."""
+    p = media.homogeneous_problem(3, 48, sponge=20, gamma_max_over_omega=1.0)
+    assert _solve(p, 3, smoother, alpha) == GOLD["table_5_4_3d"][key]["48"]
+
+
+@pytest.mark.slow
+def test_two_level_cf_close_to_lfa():
+    """P:708-713 / Fig. 5.2: the practical 2-level convergence factor (zero RHS,
+    random initial guess, c_f of Eq. 5.1) is slightly below rho_loc."""
+    n = 256
+    p = media.homogeneous_problem(2, n, sponge=20, gamma_max_over_omega=1.0)
+    opts = Options(dim=2, cells=p.cells, h=p.h, levels=2, intergrid="cubic", smoother="rb",
+                   damping=[0.83])
+    hier = build_hierarchy(opts, p.kappa, p.omega, p.gamma, 0.0)
+    f = np.zeros(p.n, complex)
+    u = media.random_complex(p.n, 7)
+    hist = [np.linalg.norm(hier.A[0] @ u)]
+    for _ in range(24):
+        u = cycle(hier, 0, f, u)
+        hist.append(np.linalg.norm(hier.A[0] @ u))
+        if hist[-1] / hist[0] < 1e-9:
+            break
+    cf = convergence_factor(np.array(hist) / hist[0], 5)
+    rho = lfa.rho_loc("rb", p.omega ** 2, p.h, 0.83)
+    assert 0.6 * rho < cf <= 1.05 * rho, (cf, rho)
