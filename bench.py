@@ -1,0 +1,322 @@
+"""Benchmark: FGMRES + additive-Vanka V-cycle time-to-solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--n 4096] [--dtype c64|c128]
+
+One STEP = one full solve H x = q from x0 = 0 to a true relative residual
+< 1e-6 (FGMRES(20) right-preconditioned by one V(1,1)-cycle, BASELINE.json
+configs[1]: 2D homogeneous, N x N cells, 10 points per wavelength, 16-node
+sponge, centre point source, log2(N) - 3 levels, alpha = 0.25).
+Setup (hmg_build_hierarchy) is excluded, as in the paper.
+
+value = unknown-updates/s = (fine unknowns x FGMRES iterations) / time-to-solve,
+summed over ranks (weak scaling: every rank solves its own replica; the slab
+partitioned solve of SURVEY §8(e) is not in this round).  Time is measured with
+CUDA events on the solve stream, barrier + synchronize on both sides, max over
+ranks.  Inputs (>= 134 MB per vector at N=4096, GBs of working set) are larger
+than the 126 MB L2.
+
+--impl reference times the CPU oracle (oracle/, SciPy, as it stands) on the
+host cores on a bounded sample of the same workload family.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FGMRES+V-cycle time-to-solve (s), unknown-updates/s, % HBM roofline @1-8 GPU"
+UNIT = "unknown-updates/s"
+ALPHA = {512: 0.25, 1024: 0.25, 2048: 0.25, 4096: 0.25}
+DAMP_RB = [0.83, 0.5, 0.4, 0.65]   # Table 5.1, last value reused
+RESTART, TOL = 20, 1e-6
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_problem(n):
+    from paper_2511_16808_b200 import media
+    return media.config_problem(1, n=n)
+
+
+def levels_for(n):
+    return max(2, n.bit_length() - 1 - 3)   # log2(N) - 3, coarsest 17^2
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    from paper_2511_16808_b200 import hmg
+    n = args.n
+    p = build_problem(n)
+    L = levels_for(n)
+    alpha = ALPHA.get(n, 0.25)
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=L, damping=DAMP_RB, dtype=args.dtype)
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    gh = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, alpha)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    cdt = torch.complex64 if args.dtype == "c64" else torch.complex128
+    q = torch.from_numpy(p.q.ravel()).to(cdt).cuda()
+    x = torch.zeros_like(q)
+    N = q.numel()
+
+    reps = []
+    for _ in range(args.warmup):
+        reps.append(gh.fgmres_solve(q, x, restart=RESTART, tol=TOL, maxiter=args.maxiter))
+    # ---------------------------------------------------------------- timed region
+    clk = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    l0 = hmg.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    its = []
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        r = gh.fgmres_solve(q, x, restart=RESTART, tol=TOL, maxiter=args.maxiter)
+        ev[k][1].record(stream)
+        its.append(r.iterations)
+        reps.append(r)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = hmg.launch_count() - l0
+    clocks = clk.stop()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    ms_step = sum(ms) / len(ms)
+    if dist:
+        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    iters = its[-1]
+    converged = all(r.converged for r in reps)
+    value = ws * N * iters / (ms_step * 1e-3)
+
+    # ---------------------------------------------------------------- e2e: host buffers through the C-ABI
+    qh = q.cpu().pin_memory()
+    xh = torch.zeros_like(qh).pin_memory()
+    e_ms = []
+    for k in range(max(1, min(args.steps, 2))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        re = gh.fgmres_solve_host(qh, xh, restart=RESTART, tol=TOL, maxiter=args.maxiter)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms.append(a.elapsed_time(b))
+    e_ms = sum(e_ms) / len(e_ms)
+    if dist:
+        t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e = {"value": ws * N * re.iterations / (e_ms * 1e-3), "unit": UNIT,
+           "time_to_solve_s": e_ms * 1e-3,
+           "h2d_bytes_per_step": qh.numel() * qh.element_size(),
+           "d2h_bytes_per_step": xh.numel() * xh.element_size()}
+
+    # ---------------------------------------------------------------- live per-kernel roofline (one extra solve)
+    hmg.profile_begin()
+    gh.fgmres_solve(q, x, restart=RESTART, tol=TOL, maxiter=args.maxiter)
+    prof = hmg.profile_report()
+    peak, peak_src = _peaks()
+    kern = sorted(prof.items(), key=lambda kv: -kv[1]["ms"])
+    tot_ms = sum(v["ms"] for v in prof.values())
+    top_name, top = kern[0]
+    per_launch_bytes = top["bytes"] / top["launches"]
+    avg_ms = top["ms"] / top["launches"]
+    achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(f"{top_name}|{args.dtype}|{n}")
+    table = {k: {"launches": v["launches"], "ms_total": round(v["ms"], 3),
+                 "share": round(v["ms"] / tot_ms, 4) if tot_ms else None,
+                 "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 else None}
+             for k, v in kern[:12]}
+    roofline = {"bound": "hbm", "kernel": top_name, "achieved": round(achieved, 1), "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_ms,
+                "share_of_step": round(top["ms"] / tot_ms, 4) if tot_ms else None}
+    # whole-solve modelled HBM fraction: algorithmic bytes of every kernel / device time
+    all_bytes = sum(v["bytes"] for v in prof.values())
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic",
+        "time_to_solve_s": ms_step * 1e-3, "iterations": iters, "converged": converged,
+        "config": {"workload": f"BASELINE configs[1]: 2D homogeneous {n}x{n} cells ({N} unknowns), 10 ppw, "
+                               f"16-node sponge, centre source, {L}-level V(1,1) RB-Vanka + lev-dep Galerkin, "
+                               f"alpha={alpha}, FGMRES({RESTART}) to {TOL}",
+                   "cells": [n, n], "levels": L, "alpha": alpha, "restart": RESTART, "tol": TOL,
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (every vector >= 134 MB at N=4096; no flush needed)",
+                   "setup_s": round(setup_s, 2)},
+        "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
+        "roofline": roofline,
+        "solve_hbm_frac_modelled": round(all_bytes / (tot_ms * 1e-3) / 1e9 / peak, 4) if tot_ms else None,
+        "kernels": table,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.cpu_n, args.cpu_iters)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+_ORACLE = {}
+
+
+def _oracle_sample(n, iters):
+    """Oracle (as it stands) on config 1 at n x n: setup untimed (built once),
+    then a fixed number of FGMRES iterations timed; returns
+    (unknown-updates/s, seconds, N, iterations)."""
+    from threadpoolctl import threadpool_limits
+    from oracle.cycle import vcycle
+    from oracle.fgmres import fgmres_solve
+    from oracle.hierarchy import Options as OOptions, build_hierarchy
+    p = build_problem(n)
+    L = levels_for(n)
+    with threadpool_limits(1):
+        if n not in _ORACLE:
+            _ORACLE[n] = build_hierarchy(OOptions(dim=2, cells=p.cells, h=p.h, levels=L, damping=DAMP_RB), p.kappa,
+                                         p.omega, p.gamma, ALPHA.get(n, 0.25))
+        oh = _ORACLE[n]
+        t0 = time.perf_counter()
+        _, info = fgmres_solve(oh.H, p.q.ravel(), lambda v: vcycle(oh, v), restart=RESTART, tol=TOL,
+                               maxiter=iters)
+        dt = time.perf_counter() - t0
+    N = p.n
+    return N * info["iterations"] / dt, dt, N, info["iterations"]
+
+
+def cpu_baseline(n, iters):
+    v, dt, N, it = _oracle_sample(n, iters)
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle (SciPy, complex128, 1 thread) on config 1 at {n}x{n} cells ({N} unknowns): "
+                      f"{it} FGMRES({RESTART}) iterations timed ({dt:.1f} s), setup excluded"}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    n = args.cpu_n
+    rates, secs = [], []
+    for k in range(args.warmup + args.steps):
+        v, dt, N, it = _oracle_sample(n, args.cpu_iters)
+        if k >= args.warmup:
+            rates.append(v)
+            secs.append(dt)
+    value = sum(rates) / len(rates)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+           "data": "synthetic",
+           "config": {"workload": f"BASELINE configs[1] family, bounded sample: {n}x{n} cells, "
+                                  f"{args.cpu_iters} FGMRES({RESTART}) iterations per step (the full N=4096 solve "
+                                  f"is hours in SciPy)", "cells": [n, n], "levels": levels_for(n)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"{n}x{n}, {args.cpu_iters} iterations per step, setup excluded"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--maxiter", type=int, default=4000)
+    ap.add_argument("--cpu-n", type=int, default=512)
+    ap.add_argument("--cpu-iters", type=int, default=40)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

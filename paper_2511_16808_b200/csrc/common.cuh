@@ -1,0 +1,120 @@
+// common.cuh -- complex arithmetic, padded-grid geometry and launch plumbing
+// shared by the libhmg CUDA sources (NOT by oracle/: the two share no code).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace hmg {
+
+// ----------------------------------------------------------------- complex
+template <typename T> struct CT;
+template <> struct CT<float>  { using type = float2; };
+template <> struct CT<double> { using type = double2; };
+template <typename T> using cplx = typename CT<T>::type;
+
+template <typename T> __host__ __device__ __forceinline__ cplx<T> mkc(T a, T b) { cplx<T> r; r.x = a; r.y = b; return r; }
+template <typename T> __host__ __device__ __forceinline__ cplx<T> cadd(cplx<T> a, cplx<T> b) { return mkc<T>(a.x + b.x, a.y + b.y); }
+template <typename T> __host__ __device__ __forceinline__ cplx<T> csub(cplx<T> a, cplx<T> b) { return mkc<T>(a.x - b.x, a.y - b.y); }
+template <typename T> __host__ __device__ __forceinline__ cplx<T> cmul(cplx<T> a, cplx<T> b) {
+  return mkc<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+template <typename T> __host__ __device__ __forceinline__ cplx<T> cscale(cplx<T> a, T s) { return mkc<T>(a.x * s, a.y * s); }
+// acc + a*b
+template <typename T> __host__ __device__ __forceinline__ cplx<T> cfma(cplx<T> acc, cplx<T> a, cplx<T> b) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+  return acc;
+}
+// acc + s*a (s real)
+template <typename T> __host__ __device__ __forceinline__ cplx<T> cfmar(cplx<T> acc, T s, cplx<T> a) {
+  acc.x = fma(s, a.x, acc.x);
+  acc.y = fma(s, a.y, acc.y);
+  return acc;
+}
+template <typename T> __host__ __device__ __forceinline__ cplx<T> cdiv(cplx<T> a, cplx<T> b) {
+  T d = b.x * b.x + b.y * b.y;
+  return mkc<T>((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+template <typename T> __host__ __device__ __forceinline__ cplx<T> crecip(cplx<T> b) {
+  T d = b.x * b.x + b.y * b.y;
+  return mkc<T>(b.x / d, -b.y / d);
+}
+template <typename T> __host__ __device__ __forceinline__ T cabs2(cplx<T> a) { return a.x * a.x + a.y * a.y; }
+
+template <typename To, typename From> __host__ __device__ __forceinline__ cplx<To> ccast(cplx<From> a) {
+  return mkc<To>((To)a.x, (To)a.y);
+}
+
+// ----------------------------------------------------------------- geometry
+// Every level vector lives in a zero-padded box: G ghost layers on each side
+// of every axis (none in z for 2D), row pitch px rounded up to 8 elements.
+// Interior node (x,y,z), 0 <= x < n[0] ..., sits at index idx(x,y,z).
+// Ghost entries are zero on one GPU, so truncation (homogeneous Dirichlet,
+// reading A4/A5) costs no branch in the operator kernels.
+struct Geo {
+  int dim;
+  int n[3];        // interior nodes per axis (n[2] = 1 in 2D)
+  int G;           // ghost width
+  int64_t px;      // row pitch
+  int64_t pxy;     // plane pitch
+  int64_t total;   // padded box size (elements)
+  int64_t base;    // index of interior node (0,0,0)
+  int64_t slab_off;  // first element of the interior slab (rows/planes G .. G+n-1)
+  int64_t slab_len;  // elements of the interior slab
+
+  __host__ __device__ __forceinline__ int64_t idx(int x, int y, int z) const {
+    return base + (int64_t)z * pxy + (int64_t)y * px + x;
+  }
+  __host__ __device__ __forceinline__ int64_t delta(int ox, int oy, int oz) const {
+    return (int64_t)oz * pxy + (int64_t)oy * px + ox;
+  }
+  __host__ __device__ __forceinline__ bool inside(int x, int y, int z) const {
+    return x >= 0 && x < n[0] && y >= 0 && y < n[1] && z >= 0 && z < n[2];
+  }
+  __host__ __device__ __forceinline__ int64_t nodes() const { return (int64_t)n[0] * n[1] * n[2]; }
+};
+
+inline Geo make_geo(int dim, const int64_t nodes[3], int G) {
+  Geo g;
+  g.dim = dim;
+  g.n[0] = (int)nodes[0];
+  g.n[1] = (int)nodes[1];
+  g.n[2] = dim == 3 ? (int)nodes[2] : 1;
+  g.G = G;
+  g.px = ((g.n[0] + 2 * G) + 7) / 8 * 8;
+  g.pxy = g.px * (g.n[1] + 2 * G);
+  int Gz = dim == 3 ? G : 0;
+  g.total = g.pxy * (g.n[2] + 2 * Gz);
+  g.base = (int64_t)Gz * g.pxy + (int64_t)G * g.px + G;
+  if (dim == 3) {
+    g.slab_off = (int64_t)G * g.pxy;
+    g.slab_len = (int64_t)g.n[2] * g.pxy;
+  } else {
+    g.slab_off = (int64_t)G * g.px;
+    g.slab_len = (int64_t)g.n[1] * g.px;
+  }
+  return g;
+}
+
+// thread -> interior node mapping used by all node-parallel kernels:
+// block (32, 8, 1), grid (ceil(nx/32), ceil(ny/8), nz)
+struct NodeLaunch {
+  dim3 grid, block;
+};
+inline NodeLaunch node_launch(const Geo &g) {
+  NodeLaunch L;
+  L.block = dim3(32, 8, 1);
+  L.grid = dim3((g.n[0] + 31) / 32, (g.n[1] + 7) / 8, g.n[2]);
+  return L;
+}
+
+// launch accounting (hmg_launch_count) -- incremented by every launch
+void count_launch();
+
+}  // namespace hmg
+
+#define HMG_NODE_IDX(g, X_, Y_, Z_)                           \
+  const int X_ = blockIdx.x * blockDim.x + threadIdx.x;       \
+  const int Y_ = blockIdx.y * blockDim.y + threadIdx.y;       \
+  const int Z_ = blockIdx.z;                                  \
+  if (X_ >= (g).n[0] || Y_ >= (g).n[1]) return;

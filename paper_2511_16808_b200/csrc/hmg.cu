@@ -1,0 +1,1079 @@
+// hmg.cu -- host orchestration and the extern "C" boundary of libhmg.so.
+//
+// Hot path: FGMRES(m) right-preconditioned by one
+// multigrid cycle (Alg. 2.1) on the shifted operator H_s (Eq. 2.6)
+// with additive Vanka smoothing (Eq. 3.8), Galerkin coarse operators
+// and level-dependent intergrid (Eqs. 3.3-3.4).  Every arithmetic
+// step runs in the kernels of k_*.cuh; this file only sequences launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hmg.h"
+#include "common.cuh"
+#include "k_krylov.cuh"
+#include "k_operator.cuh"
+#include "k_setup.cuh"
+#include "k_transfer.cuh"
+#include "k_vanka.cuh"
+
+namespace hmg {
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct HmgError : std::runtime_error {
+  hmg_status st;
+  HmgError(hmg_status s, const std::string &m) : std::runtime_error(m), st(s) {}
+};
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      throw HmgError(e_ == cudaErrorMemoryAllocation ? HMG_ENOMEM : HMG_ECUDA,                     \
+                     std::string(#call) + ": " + cudaGetErrorString(e_));                          \
+  } while (0)
+
+// ---- opt-in per-kernel profiling (hmg_profile_begin / hmg_profile_report):
+// every solve-path launch is tagged with a kernel class, its level and its
+// ALGORITHMIC bytes (DESIGN.md bytes model); when profiling is on, CUDA events
+// bracket each launch on its own stream.
+struct ProfRec {
+  std::string name;
+  double bytes;
+  cudaEvent_t a, b;
+};
+struct Profiler {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  size_t used = 0;
+};
+static Profiler g_prof;
+static thread_local const char *t_name = nullptr;
+static thread_local int t_level = 0;
+static thread_local double t_bytes = 0;
+static void tag(const char *name, int level, double bytes) {
+  t_name = name;
+  t_level = level;
+  t_bytes = bytes;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args... args) {
+  if (g.x == 0 || g.y == 0 || g.z == 0) return;
+  const bool prof = g_prof.on && t_name;
+  cudaEvent_t ea = nullptr, eb = nullptr;
+  if (prof) {
+    if (g_prof.used == g_prof.pool.size()) {
+      cudaEvent_t x, y;
+      CK(cudaEventCreate(&x));
+      CK(cudaEventCreate(&y));
+      g_prof.pool.emplace_back(x, y);
+    }
+    ea = g_prof.pool[g_prof.used].first;
+    eb = g_prof.pool[g_prof.used].second;
+    ++g_prof.used;
+    CK(cudaEventRecord(ea, s));
+  }
+  k<<<g, b, smem, s>>>(static_cast<KArgs>(args)...);
+  count_launch();
+  CK(cudaGetLastError());
+  if (prof) {
+    CK(cudaEventRecord(eb, s));
+    g_prof.recs.push_back({std::string(t_name) + "@L" + std::to_string(t_level), t_bytes, ea, eb});
+  }
+  t_name = nullptr;
+}
+
+struct DBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf &operator=(DBuf &&o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t n, cudaStream_t s) {
+    release();
+    if (n == 0) n = 16;
+    CK(cudaMalloc(&p, n));
+    bytes = n;
+    CK(cudaMemsetAsync(p, 0, n, s));
+  }
+  template <typename X> X *as() const { return reinterpret_cast<X *>(p); }
+};
+
+// transfer radii for level l -> l+1
+static void level_scheme(int scheme, int l, int &rR, int &rP) {
+  switch (scheme) {
+    case HMG_LEVDEP: rR = l == 0 ? 2 : 1; rP = 2; break;
+    case HMG_LINEAR: rR = 1; rP = 1; break;
+    case HMG_CUBIC: rR = 2; rP = 2; break;
+    case HMG_MIXED: rR = 1; rP = 2; break;
+    default: throw HmgError(HMG_EINVAL, "unknown intergrid scheme");
+  }
+}
+
+static TransferW transfer_weights(int rR, int rP) {
+  TransferW t{};
+  t.rR = rR;
+  t.rP = rP;
+  const double lin[3] = {0.25, 0.5, 0.25};
+  const double cub[5] = {1.0 / 16, 4.0 / 16, 6.0 / 16, 4.0 / 16, 1.0 / 16};
+  for (int k = 0; k < 2 * rR + 1; ++k) t.wR[k] = rR == 1 ? lin[k] : cub[k];
+  for (int k = 0; k < 2 * rP + 1; ++k) t.wP[k] = rP == 1 ? lin[k] : cub[k];
+  return t;
+}
+
+static int patch_size(int dim, int kind) {
+  switch (kind) {
+    case HMG_JACOBI: return 1;
+    case HMG_VANKA_ELEMENT: return 1 << dim;
+    case HMG_VANKA_PLUS: return 2 * dim + 1;
+    case HMG_VANKA_RB: return 5;
+  }
+  return 0;
+}
+
+__global__ void k_identity(int N, double2 *__restrict__ A) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < (int64_t)N * N) A[i] = make_double2((i / N) == (i % N) ? 1.0 : 0.0, 0.0);
+}
+
+template <typename T> __global__ void k_coarse_gemv(Geo g, const double2 *__restrict__ Ainv,
+                                                    const cplx<T> *__restrict__ r, cplx<T> *__restrict__ e) {
+  const int N = (int)g.nodes();
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= N) return;
+  double ax = 0, ay = 0;
+  for (int col = lane; col < N; col += 32) {
+    const int cx = col % g.n[0], cy = (col / g.n[0]) % g.n[1], cz = col / (g.n[0] * g.n[1]);
+    const cplx<T> v = r[g.idx(cx, cy, cz)];
+    const double2 a = Ainv[(int64_t)row * N + col];
+    ax = fma(a.x, (double)v.x, fma(-a.y, (double)v.y, ax));
+    ay = fma(a.x, (double)v.y, fma(a.y, (double)v.x, ay));
+  }
+  ax = warp_sum(ax);
+  ay = warp_sum(ay);
+  if (lane == 0) {
+    const int rx = row % g.n[0], ry = (row / g.n[0]) % g.n[1], rz = row / (g.n[0] * g.n[1]);
+    e[g.idx(rx, ry, rz)] = mkc<T>((T)ax, (T)ay);
+  }
+}
+
+struct SolverBase {
+  virtual ~SolverBase() = default;
+  hmg_options opt{};
+  std::vector<double> damping;
+  int L = 0;
+  virtual void build(const double *kappa, double omega, const double *gamma, double alpha, cudaStream_t s) = 0;
+  virtual void api_apply(int level, int shifted, const void *x, void *y, cudaStream_t s) = 0;
+  virtual void api_residual(int level, int shifted, const void *f, const void *x, void *r, cudaStream_t s) = 0;
+  virtual void api_smooth(int level, const void *f, void *u, cudaStream_t s) = 0;
+  virtual void api_restrict(int level, const void *r, void *fc, cudaStream_t s) = 0;
+  virtual void api_prolong(int level, const void *ec, void *u, cudaStream_t s) = 0;
+  virtual void api_coarse(const void *r, void *e, cudaStream_t s) = 0;
+  virtual void api_vcycle(const void *f, void *x, int zero, cudaStream_t s) = 0;
+  virtual hmg_status api_fgmres(const void *q, void *x, int host, int restart, double tol, int maxiter,
+                                cudaStream_t s, hmg_report *rep) = 0;
+  virtual int64_t level_nodes(int level, int64_t n[3]) const = 0;
+  virtual int radius(int level) const = 0;
+  virtual int copy_stencil(int level, double *out, int64_t cap) = 0;
+};
+
+template <typename T> struct Solver : SolverBase {
+  using C = cplx<T>;
+  struct Level {
+    Geo geo;
+    double h = 0;
+    int r = 1;      // stored stencil radius
+    int rR = 0, rP = 0;
+    DBuf coef;      // C [K][total] (levels > 0)
+    DBuf hinv;      // C [k*k][total] (generic patch solve)
+    DBuf u, f, r_, y;
+  };
+  std::vector<Level> lev;
+  int G = 2;
+  double omega = 0, alpha = 0;
+  DBuf sig, w2k2, gq;     // fine-level coefficients
+  DBuf sigd;              // fine-level sigma in fp64 (restart residual of FGMRES)
+  DBuf ainv;              // coarsest inverse, double2 N_L x N_L
+  bool rb_closed = false; // fine level uses the closed-form RB patch solve
+  // FGMRES workspace
+  int ws_m = 0;
+  DBuf V, Z, partial, dres, io;
+  DBuf qd, xd, rd;        // fp64 right-hand side, iterate and restart residual
+  int nblk = 0;
+  double *hpin = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  ~Solver() override {
+    if (hpin) cudaFreeHost(hpin);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+  }
+
+  const Geo &g0() const { return lev[0].geo; }
+  double damp(int l) const { return damping[std::min<size_t>(l, damping.size() - 1)]; }
+
+  // ------------------------------------------------------------------ build
+  void build(const double *kappa, double omega_, const double *gamma, double alpha_, cudaStream_t s) override {
+    omega = omega_;
+    alpha = alpha_;
+    const int dim = opt.dim;
+    L = opt.levels;
+    G = opt.intergrid == HMG_CUBIC ? 3 : 2;
+    lev.resize(L);
+    int64_t nodes[3] = {opt.cells[0] + 1, opt.cells[1] + 1, dim == 3 ? opt.cells[2] + 1 : 1};
+    double h = opt.h;
+    for (int l = 0; l < L; ++l) {
+      lev[l].geo = make_geo(dim, nodes, G);
+      lev[l].h = h;
+      for (int a = 0; a < dim; ++a) nodes[a] = (nodes[a] - 1) / 2 + 1;
+      h *= 2;
+    }
+    const Geo &f0 = lev[0].geo;
+    const int64_t N0 = f0.nodes();
+    // a1: coefficients
+    {
+      DBuf dk, dg;
+      dk.alloc(N0 * sizeof(double), s);
+      dg.alloc(N0 * sizeof(double), s);
+      CK(cudaMemcpyAsync(dk.p, kappa, N0 * sizeof(double), cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dg.p, gamma, N0 * sizeof(double), cudaMemcpyHostToDevice, s));
+      w2k2.alloc(f0.total * sizeof(double), s);
+      gq.alloc(f0.total * sizeof(double), s);
+      sig.alloc(f0.total * sizeof(C), s);
+      sigd.alloc(f0.total * sizeof(double2), s);
+      auto nl = node_launch(f0);
+      launch(k_sigma<T>, nl.grid, nl.block, 0, s, f0, dk.template as<double>(), dg.template as<double>(), omega, w2k2.template as<double>(),
+             gq.template as<double>(), sig.template as<C>(), sigd.template as<double2>());
+      CK(cudaStreamSynchronize(s));
+    }
+    // level operators in fp64
+    std::vector<DBuf> cd(L);
+    lev[0].r = 1;
+    materialize(lev[0].geo, lev[0].h, w2k2.template as<double>(), gq.template as<double>(), cd[0], s);
+    DBuf cw, cg;  // REDISCRETIZE coarse fields
+    const double *pw = w2k2.template as<double>(), *pg = gq.template as<double>();
+    for (int l = 0; l + 1 < L; ++l) {
+      Level &F = lev[l], &Cc = lev[l + 1];
+      level_scheme(opt.intergrid, l, F.rR, F.rP);
+      if (opt.coarse_op == HMG_GALERKIN) {
+        const int rc = (F.rR + F.r + F.rP) / 2;
+        if (rc > G) throw HmgError(HMG_EINVAL, "coarse stencil radius exceeds ghost width");
+        if (dim == 3 && rc > 2) throw HmgError(HMG_EINVAL, "CUBIC intergrid is supported in 2D only");
+        Cc.r = rc;
+        const int K = kcount(dim, rc);
+        cd[l + 1].alloc((size_t)K * Cc.geo.total * sizeof(double2), s);
+        TransferW tw = transfer_weights(F.rR, F.rP);
+        auto nl = node_launch(Cc.geo);
+        if (dim == 2) {
+          if (rc == 1) launch(k_galerkin<2, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+          else if (rc == 2) launch(k_galerkin<2, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+          else launch(k_galerkin<2, 3>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+        } else {
+          if (rc == 1) launch(k_galerkin<3, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+          else launch(k_galerkin<3, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+        }
+      } else {
+        DBuf nw, ng;
+        nw.alloc(Cc.geo.total * sizeof(double), s);
+        ng.alloc(Cc.geo.total * sizeof(double), s);
+        auto nl = node_launch(Cc.geo);
+        launch(k_fw_average, nl.grid, nl.block, 0, s, F.geo, Cc.geo, pw, nw.template as<double>());
+        launch(k_fw_average, nl.grid, nl.block, 0, s, F.geo, Cc.geo, pg, ng.template as<double>());
+        CK(cudaStreamSynchronize(s));
+        cw = std::move(nw);
+        cg = std::move(ng);
+        pw = cw.template as<double>();
+        pg = cg.template as<double>();
+        Cc.r = 1;
+        materialize(Cc.geo, Cc.h, pw, pg, cd[l + 1], s);
+      }
+      CK(cudaStreamSynchronize(s));
+    }
+    // stored stencils in the working precision (levels > 0)
+    for (int l = 1; l < L; ++l) {
+      Level &Lv = lev[l];
+      const int64_t n = (int64_t)kcount(dim, Lv.r) * Lv.geo.total;
+      Lv.coef.alloc(n * sizeof(C), s);
+      launch(k_cast<T>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, cd[l].template as<double2>(), Lv.coef.template as<C>(), n);
+    }
+    // Vanka patch factors
+    rb_closed = (dim == 2 && opt.smoother == HMG_VANKA_RB);
+    DBuf errb;
+    errb.alloc(sizeof(unsigned long long), s);
+    for (int l = 0; l + 1 < L; ++l) {
+      Level &Lv = lev[l];
+      const int k = patch_size(dim, opt.smoother);
+      Lv.y.alloc((size_t)k * Lv.geo.total * sizeof(C), s);
+      if (l == 0 && rb_closed) continue;
+      Lv.hinv.alloc((size_t)k * k * Lv.geo.total * sizeof(C), s);
+      CK(cudaMemsetAsync(errb.p, 0xff, sizeof(unsigned long long), s));
+      patch_inverse(Lv, cd[l], errb.template as<unsigned long long>(), s);
+      unsigned long long bad = 0;
+      CK(cudaMemcpyAsync(&bad, errb.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (bad != ~0ull) {
+        const int64_t nx = Lv.geo.n[0], ny = Lv.geo.n[1];
+        char buf[160];
+        snprintf(buf, sizeof buf, "singular Vanka patch at level %d, anchor node (%lld, %lld, %lld)", l,
+                 (long long)(bad % nx), (long long)((bad / nx) % ny), (long long)(bad / (nx * ny)));
+        throw HmgError(HMG_ESINGULAR_PATCH, buf);
+      }
+    }
+    // coarsest dense inverse (fp64)
+    {
+      Level &Lc = lev[L - 1];
+      const int N = (int)Lc.geo.nodes();
+      if ((int64_t)N * N * 16 > (int64_t)8 << 30) throw HmgError(HMG_EINVAL, "coarsest level too large for a dense inverse");
+      DBuf A, fcol, err;
+      A.alloc((size_t)N * N * sizeof(double2), s);
+      ainv.alloc((size_t)N * N * sizeof(double2), s);
+      fcol.alloc((size_t)N * sizeof(double2), s);
+      err.alloc(sizeof(int), s);
+      auto nl = node_launch(Lc.geo);
+      launch(k_dense_assemble, nl.grid, nl.block, 0, s, Lc.geo, cd[L - 1].template as<double2>(), Lc.r, A.template as<double2>());
+      launch(k_identity, dim3((unsigned)(((int64_t)N * N + 255) / 256)), dim3(256), 0, s, N, ainv.template as<double2>());
+      for (int k = 0; k < N; ++k) {
+        launch(k_gj_pivot, dim3(1), dim3(1024), 0, s, N, k, A.template as<double2>(), ainv.template as<double2>(), fcol.template as<double2>(), err.template as<int>());
+        launch(k_gj_eliminate, dim3((N + 255) / 256, N), dim3(256), 0, s, N, k, A.template as<double2>(), ainv.template as<double2>(),
+               fcol.template as<double2>());
+      }
+      int bad = 0;
+      CK(cudaMemcpyAsync(&bad, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (bad) throw HmgError(HMG_ESINGULAR_COARSE, "coarsest Galerkin matrix is singular");
+    }
+    // cycle workspace
+    for (int l = 0; l < L; ++l) {
+      Level &Lv = lev[l];
+      Lv.u.alloc(Lv.geo.total * sizeof(C), s);
+      Lv.f.alloc(Lv.geo.total * sizeof(C), s);
+      Lv.r_.alloc(Lv.geo.total * sizeof(C), s);
+    }
+    io.alloc((size_t)N0 * sizeof(C), s);
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaMallocHost((void **)&hpin, 4096 * sizeof(double)));
+    CK(cudaStreamSynchronize(s));
+  }
+
+  static int kcount(int dim, int r) { return dim == 3 ? (2 * r + 1) * (2 * r + 1) * (2 * r + 1) : (2 * r + 1) * (2 * r + 1); }
+
+  void materialize(const Geo &g, double h, const double *pw, const double *pg, DBuf &out, cudaStream_t s) {
+    const int K = kcount(opt.dim, 1);
+    out.alloc((size_t)K * g.total * sizeof(double2), s);
+    auto nl = node_launch(g);
+    const double ih2 = 1.0 / (h * h);
+    const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+    if (opt.dim == 2) {
+      if (c4) launch(k_materialize<2, ST_COMPACT4>, nl.grid, nl.block, 0, s, g, pw, pg, alpha, ih2, out.template as<double2>());
+      else launch(k_materialize<2, ST_FD2>, nl.grid, nl.block, 0, s, g, pw, pg, alpha, ih2, out.template as<double2>());
+    } else {
+      if (c4) launch(k_materialize<3, ST_COMPACT4>, nl.grid, nl.block, 0, s, g, pw, pg, alpha, ih2, out.template as<double2>());
+      else launch(k_materialize<3, ST_FD2>, nl.grid, nl.block, 0, s, g, pw, pg, alpha, ih2, out.template as<double2>());
+    }
+  }
+
+  void patch_inverse(Level &Lv, DBuf &cd, unsigned long long *err, cudaStream_t s) {
+    auto nl = node_launch(Lv.geo);
+    const double2 *c = cd.template as<double2>();
+    C *hv = Lv.hinv.template as<C>();
+    const int dim = opt.dim;
+    switch (opt.smoother) {
+      case HMG_VANKA_RB:
+        if (dim != 2) throw HmgError(HMG_EINVAL, "RB patch is 2D only (the paper rejects the 13-node 3D RB patch, P:949-951)");
+        launch(k_patch_inverse<T, 2, PK_RB>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        break;
+      case HMG_VANKA_ELEMENT:
+        if (dim == 2) launch(k_patch_inverse<T, 2, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        else launch(k_patch_inverse<T, 3, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        break;
+      case HMG_JACOBI:
+        if (dim == 2) launch(k_patch_inverse<T, 2, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        else launch(k_patch_inverse<T, 3, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        break;
+      case HMG_VANKA_PLUS:
+        if (dim == 2) launch(k_patch_inverse<T, 2, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        else launch(k_patch_inverse<T, 3, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        break;
+      default: throw HmgError(HMG_EINVAL, "unknown smoother");
+    }
+  }
+
+  // ------------------------------------------------------------ operators
+  // y = A_l x  or  y = f - A_l x
+  void op(int l, int shifted, const C *x, const C *f, C *y, cudaStream_t s) {
+    const Level &Lv = lev[l];
+    auto nl = node_launch(Lv.geo);
+    const double sz = sizeof(C), nn = (double)Lv.geo.nodes();
+    if (l == 0) {
+      tag(f ? "fine_residual" : "fine_apply", l, (f ? 4 : 3) * sz * nn);
+      const T a = shifted ? (T)alpha : (T)0;
+      const T ih2 = (T)(1.0 / (Lv.h * Lv.h));
+      const C *sg = sig.template as<C>();
+      const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+      if (opt.dim == 2) {
+        if (c4) launch(k_fine_op<T, 2, ST_COMPACT4>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, x, f, y);
+        else launch(k_fine_op<T, 2, ST_FD2>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, x, f, y);
+      } else {
+        if (c4) launch(k_fine_op<T, 3, ST_COMPACT4>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, x, f, y);
+        else launch(k_fine_op<T, 3, ST_FD2>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, x, f, y);
+      }
+      return;
+    }
+    const C *cf = Lv.coef.template as<C>();
+    tag(f ? "stored_residual" : "stored_apply", l, (kcount(opt.dim, Lv.r) + (f ? 3 : 2)) * sz * nn);
+    if (opt.dim == 2) {
+      if (Lv.r == 1) launch(k_stored_op<T, 2, 1>, nl.grid, nl.block, 0, s, Lv.geo, cf, x, f, y);
+      else if (Lv.r == 2) launch(k_stored_op<T, 2, 2>, nl.grid, nl.block, 0, s, Lv.geo, cf, x, f, y);
+      else launch(k_stored_op<T, 2, 3>, nl.grid, nl.block, 0, s, Lv.geo, cf, x, f, y);
+    } else {
+      if (Lv.r == 1) launch(k_stored_op<T, 3, 1>, nl.grid, nl.block, 0, s, Lv.geo, cf, x, f, y);
+      else launch(k_stored_op<T, 3, 2>, nl.grid, nl.block, 0, s, Lv.geo, cf, x, f, y);
+    }
+  }
+
+  void restrict_(int l, const C *r, C *fc, cudaStream_t s) {
+    const Level &F = lev[l], &Cc = lev[l + 1];
+    auto nl = node_launch(Cc.geo);
+    tag("restrict", l, (double)sizeof(C) * (F.geo.nodes() + Cc.geo.nodes()));
+    if (opt.dim == 2) {
+      if (F.rR == 1) launch(k_restrict<T, 2, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, r, fc);
+      else launch(k_restrict<T, 2, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, r, fc);
+    } else {
+      if (F.rR == 1) launch(k_restrict<T, 3, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, r, fc);
+      else launch(k_restrict<T, 3, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, r, fc);
+    }
+  }
+
+  void prolong_(int l, const C *e, C *u, cudaStream_t s) {
+    const Level &F = lev[l], &Cc = lev[l + 1];
+    auto nl = node_launch(F.geo);
+    tag("prolong_add", l, (double)sizeof(C) * (2 * F.geo.nodes() + Cc.geo.nodes()));
+    if (opt.dim == 2) {
+      if (F.rP == 1) launch(k_prolong_add<T, 2, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u);
+      else launch(k_prolong_add<T, 2, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u);
+    } else {
+      if (F.rP == 1) launch(k_prolong_add<T, 3, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u);
+      else launch(k_prolong_add<T, 3, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u);
+    }
+  }
+
+  template <int DIM, int KIND> void vanka_(Level &Lv, const C *r, C *u, T w, int zero, cudaStream_t s) {
+    auto nl = node_launch(Lv.geo);
+    C *y = Lv.y.template as<C>();
+    constexpr int K = Patch<DIM, KIND>::K;
+    const double sz = sizeof(C), nn = (double)Lv.geo.nodes();
+    tag("patch_apply", (int)(&Lv - lev.data()), (K * K + K + 1) * sz * nn);
+    launch(k_patch_apply<T, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, Lv.hinv.template as<C>(), r, y);
+    tag("vanka_gather", (int)(&Lv - lev.data()), (K + (zero ? 1 : 2)) * sz * nn);
+    launch(k_vanka_gather<T, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)y, w, u, zero);
+  }
+
+  // one additive Vanka relaxation u <- u + w B (f - A u); zero: u == 0 on input
+  void smooth(int l, const C *f, C *u, int zero, cudaStream_t s) {
+    Level &Lv = lev[l];
+    const C *r = f;
+    if (!zero) {
+      op(l, 1, u, f, Lv.r_.template as<C>(), s);
+      r = Lv.r_.template as<C>();
+    }
+    const T w = (T)damp(l);
+    if (l == 0 && rb_closed) {
+      auto nl = node_launch(Lv.geo);
+      const T ih2 = (T)(1.0 / (Lv.h * Lv.h));
+      C *y = Lv.y.template as<C>();
+      const double sz = sizeof(C), nn = (double)Lv.geo.nodes();
+      tag("patch_rb2d_fine", 0, 7 * sz * nn);
+      if (opt.fine_stencil == HMG_COMPACT4)
+        launch(k_patch_rb2d_fine<T, ST_COMPACT4>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)sig.template as<C>(), (T)alpha, ih2, r, y);
+      else
+        launch(k_patch_rb2d_fine<T, ST_FD2>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)sig.template as<C>(), (T)alpha, ih2, r, y);
+      tag("vanka_gather", 0, (5 + (zero ? 1 : 2)) * sz * nn);
+      launch(k_vanka_gather<T, 2, PK_RB>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)y, w, u, zero);
+      return;
+    }
+    const int dim = opt.dim;
+    switch (opt.smoother) {
+      case HMG_VANKA_RB: vanka_<2, PK_RB>(Lv, r, u, w, zero, s); break;
+      case HMG_VANKA_ELEMENT: dim == 2 ? vanka_<2, PK_ELEMENT>(Lv, r, u, w, zero, s) : vanka_<3, PK_ELEMENT>(Lv, r, u, w, zero, s); break;
+      case HMG_JACOBI: dim == 2 ? vanka_<2, PK_JACOBI>(Lv, r, u, w, zero, s) : vanka_<3, PK_JACOBI>(Lv, r, u, w, zero, s); break;
+      case HMG_VANKA_PLUS: dim == 2 ? vanka_<2, PK_PLUS>(Lv, r, u, w, zero, s) : vanka_<3, PK_PLUS>(Lv, r, u, w, zero, s); break;
+    }
+  }
+
+  void coarse_(const C *r, C *e, cudaStream_t s) {
+    const Level &Lc = lev[L - 1];
+    const int N = (int)Lc.geo.nodes();
+    tag("coarse_gemv", L - 1, (double)N * N * 16 + 2.0 * N * sizeof(C));
+    launch(k_coarse_gemv<T>, dim3((N + 7) / 8), dim3(256), 0, s, Lc.geo, (const double2 *)ainv.template as<double2>(), r, e);
+  }
+
+  // Alg. 2.1, recursive; u <- MG_l(f, u)
+  void cycle(int l, const C *f, C *u, int zero, cudaStream_t s) {
+    if (l == L - 1) {
+      coarse_(f, u, s);
+      return;
+    }
+    Level &Lv = lev[l];
+    for (int k = 0; k < opt.nu1; ++k) smooth(l, f, u, zero && k == 0, s);
+    if (opt.nu1 == 0 && zero) CK(cudaMemsetAsync(u, 0, Lv.geo.total * sizeof(C), s));
+    op(l, 1, u, f, Lv.r_.template as<C>(), s);                         // step 2: r = f - A u
+    Level &Cc = lev[l + 1];
+    restrict_(l, Lv.r_.template as<C>(), Cc.f.template as<C>(), s);             //         f_c = R r
+    const int rec = opt.cycle == 1 ? 2 : 1;                   // step 3: V / W recursion
+    for (int c = 0; c < rec; ++c) cycle(l + 1, Cc.f.template as<C>(), Cc.u.template as<C>(), c == 0, s);
+    prolong_(l, Cc.u.template as<C>(), u, s);                          // step 4: u += P e
+    for (int k = 0; k < opt.nu2; ++k) smooth(l, f, u, 0, s);  // step 5
+  }
+
+  // ------------------------------------------------------------ API glue
+  void pack(int l, const void *src, C *dst, cudaStream_t s) {
+    auto nl = node_launch(lev[l].geo);
+    tag("pack", l, 2.0 * sizeof(C) * lev[l].geo.nodes());
+    launch(k_pack<C>, nl.grid, nl.block, 0, s, lev[l].geo, (const C *)src, dst);
+  }
+  void unpack(int l, const C *src, void *dst, cudaStream_t s) {
+    auto nl = node_launch(lev[l].geo);
+    tag("unpack", l, 2.0 * sizeof(C) * lev[l].geo.nodes());
+    launch(k_unpack<C>, nl.grid, nl.block, 0, s, lev[l].geo, src, (C *)dst);
+  }
+  void check_level(int l, bool allow_coarsest = true) const {
+    if (l < 0 || l >= L || (!allow_coarsest && l == L - 1)) throw HmgError(HMG_EINVAL, "level out of range");
+  }
+  void api_apply(int l, int shifted, const void *x, void *y, cudaStream_t s) override {
+    check_level(l);
+    if (l > 0 && !shifted) throw HmgError(HMG_EINVAL, "coarse levels hold the shifted operator only");
+    Level &Lv = lev[l];
+    pack(l, x, Lv.u.template as<C>(), s);
+    op(l, shifted, Lv.u.template as<C>(), nullptr, Lv.r_.template as<C>(), s);
+    unpack(l, Lv.r_.template as<C>(), y, s);
+  }
+  void api_residual(int l, int shifted, const void *f, const void *x, void *r, cudaStream_t s) override {
+    check_level(l);
+    if (l > 0 && !shifted) throw HmgError(HMG_EINVAL, "coarse levels hold the shifted operator only");
+    Level &Lv = lev[l];
+    pack(l, f, Lv.f.template as<C>(), s);
+    pack(l, x, Lv.u.template as<C>(), s);
+    op(l, shifted, Lv.u.template as<C>(), Lv.f.template as<C>(), Lv.r_.template as<C>(), s);
+    unpack(l, Lv.r_.template as<C>(), r, s);
+  }
+  void api_smooth(int l, const void *f, void *u, cudaStream_t s) override {
+    check_level(l, false);
+    Level &Lv = lev[l];
+    pack(l, f, Lv.f.template as<C>(), s);
+    pack(l, u, Lv.u.template as<C>(), s);
+    smooth(l, Lv.f.template as<C>(), Lv.u.template as<C>(), 0, s);
+    unpack(l, Lv.u.template as<C>(), u, s);
+  }
+  void api_restrict(int l, const void *r, void *fc, cudaStream_t s) override {
+    check_level(l, false);
+    pack(l, r, lev[l].r_.template as<C>(), s);
+    restrict_(l, lev[l].r_.template as<C>(), lev[l + 1].f.template as<C>(), s);
+    unpack(l + 1, lev[l + 1].f.template as<C>(), fc, s);
+  }
+  void api_prolong(int l, const void *ec, void *u, cudaStream_t s) override {
+    check_level(l, false);
+    pack(l + 1, ec, lev[l + 1].u.template as<C>(), s);
+    pack(l, u, lev[l].u.template as<C>(), s);
+    prolong_(l, lev[l + 1].u.template as<C>(), lev[l].u.template as<C>(), s);
+    unpack(l, lev[l].u.template as<C>(), u, s);
+  }
+  void api_coarse(const void *r, void *e, cudaStream_t s) override {
+    Level &Lc = lev[L - 1];
+    pack(L - 1, r, Lc.f.template as<C>(), s);
+    coarse_(Lc.f.template as<C>(), Lc.u.template as<C>(), s);
+    unpack(L - 1, Lc.u.template as<C>(), e, s);
+  }
+  void api_vcycle(const void *f, void *x, int zero, cudaStream_t s) override {
+    Level &Lv = lev[0];
+    pack(0, f, Lv.f.template as<C>(), s);
+    if (!zero) pack(0, x, Lv.u.template as<C>(), s);
+    cycle(0, Lv.f.template as<C>(), Lv.u.template as<C>(), zero, s);
+    unpack(0, Lv.u.template as<C>(), x, s);
+  }
+
+  // ------------------------------------------------------------ FGMRES
+  // Mixed precision (both dtypes): the Arnoldi basis V, the preconditioned
+  // vectors Z and every V-cycle run in the working precision T; the iterate x,
+  // the right-hand side and the residual r = q - H x formed at each restart
+  // are fp64.  For T = double this is plain FGMRES; for T = float it lets the
+  // true relative residual reach 1e-6 although fp32 rounding of H x alone is
+  // ~1e-6 relative for these operators (restarted GMRES as iterative
+  // refinement).  Dots accumulate in fp64 in every case.
+  void ensure_ws(int m, cudaStream_t s) {
+    if (ws_m == m) return;
+    const Geo &g = g0();
+    V.alloc((size_t)(m + 1) * g.total * sizeof(C), s);
+    Z.alloc((size_t)m * g.total * sizeof(C), s);
+    nblk = (int)std::min<int64_t>(148 * 8, (g.slab_len + KRY_THREADS - 1) / KRY_THREADS);
+    partial.alloc((size_t)KRY_MAXV * nblk * sizeof(double2), s);
+    dres.alloc(256 * sizeof(double2), s);
+    if (!qd.p) {
+      qd.alloc(g.total * sizeof(double2), s);
+      xd.alloc(g.total * sizeof(double2), s);
+      rd.alloc(g.total * sizeof(double2), s);
+    }
+    ws_m = m;
+  }
+  C *Vp(int i) { return V.template as<C>() + (size_t)i * g0().total; }
+  C *Zp(int i) { return Z.template as<C>() + (size_t)i * g0().total; }
+
+  // out[0..nv) = V_i^H w over the interior slab
+  template <typename TV, typename TW>
+  void mdot(const cplx<TV> *Vb, int nv, const cplx<TW> *w, double2 *out, cudaStream_t s) {
+    const Geo &g = g0();
+    tag("multidot", 0, (nv * sizeof(cplx<TV>) + sizeof(cplx<TW>)) * (double)g.slab_len);
+    launch(k_multidot<TV, TW>, dim3(nblk), dim3(KRY_THREADS), 0, s, Vb + g.slab_off, g.total, nv, w + g.slab_off,
+           g.slab_len, partial.template as<double2>());
+    tag("reduce", 0, 16.0 * nv * nblk);
+    launch(k_reduce_partials, dim3(nv), dim3(32), 0, s, (const double2 *)partial.template as<double2>(), nblk, nv, out);
+  }
+  template <typename TV, typename TW>
+  void maxpy(const cplx<TV> *Vb, int nv, const double2 *coef, double sgn, cplx<TW> *w, double2 *nrm_out,
+             cudaStream_t s) {
+    const Geo &g = g0();
+    tag("multi_axpy", 0, (nv * sizeof(cplx<TV>) + 2.0 * sizeof(cplx<TW>)) * (double)g.slab_len);
+    launch(k_multi_axpy<TV, TW>, dim3(nblk), dim3(KRY_THREADS), 0, s, Vb + g.slab_off, g.total, nv, coef, sgn,
+           w + g.slab_off, g.slab_len, nrm_out ? partial.template as<double2>() : (double2 *)nullptr);
+    if (nrm_out) {
+      tag("reduce", 0, 16.0 * nblk);
+      launch(k_reduce_partials, dim3(1), dim3(32), 0, s, (const double2 *)partial.template as<double2>(), nblk, 1,
+             nrm_out);
+    }
+  }
+  template <typename TX> double norm(const cplx<TX> *x, cudaStream_t s) {
+    double2 *d = dres.template as<double2>() + 200;
+    mdot<TX, TX>(x, 1, x, d, s);
+    double2 hv;
+    CK(cudaMemcpyAsync(&hv, d, sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return std::sqrt(std::max(hv.x, 0.0));
+  }
+  template <typename TI, typename TO> void scale(const cplx<TI> *w, cplx<TO> *v, double a, cudaStream_t s) {
+    const Geo &g = g0();
+    tag("scale", 0, (sizeof(cplx<TI>) + sizeof(cplx<TO>)) * (double)g.slab_len);
+    launch(k_scale<TI, TO>, dim3(nblk), dim3(KRY_THREADS), 0, s, w + g.slab_off, v + g.slab_off, a, g.slab_len);
+  }
+  // rd = qd - H xd in fp64 (unshifted fine operator)
+  void residual_d(cudaStream_t s) {
+    const Level &Lv = lev[0];
+    auto nl = node_launch(Lv.geo);
+    const double ih2 = 1.0 / (Lv.h * Lv.h);
+    const double2 *sg = sigd.template as<double2>();
+    const double2 *x = xd.template as<double2>(), *f = qd.template as<double2>();
+    double2 *y = rd.template as<double2>();
+    tag("fine_residual_fp64", 0, 64.0 * Lv.geo.nodes());
+    const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+    if (opt.dim == 2) {
+      if (c4) launch(k_fine_op<double, 2, ST_COMPACT4>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y);
+      else launch(k_fine_op<double, 2, ST_FD2>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y);
+    } else {
+      if (c4) launch(k_fine_op<double, 3, ST_COMPACT4>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y);
+      else launch(k_fine_op<double, 3, ST_FD2>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y);
+    }
+  }
+
+  // Saad's FGMRES(m) with CGS2 Arnoldi and complex Givens rotations; x0 = 0;
+  // stop when |g_{j+1}|/||q|| < tol and the fp64 true residual confirms it
+  // (reading A17), else restart.  Solves qd -> xd.
+  hmg_status fgmres(int m, double tol, int maxiter, cudaStream_t s, std::vector<double> &hist, int &its_out,
+                    int &restarts_out, double &true_rel_out, double &est_out) {
+    typedef std::complex<double> cd;
+    ensure_ws(m, s);
+    const Geo &g = g0();
+    double2 *x = xd.template as<double2>();
+    CK(cudaMemsetAsync(x, 0, g.total * sizeof(double2), s));
+    const double qn = norm<double>(qd.template as<double2>(), s);
+    hist.assign(1, 1.0);
+    int its = 0, restarts = 0;
+    bool converged = false;
+    double true_rel = 1.0, est = 1.0;
+    if (qn == 0.0) {
+      its_out = 0; restarts_out = 0; true_rel_out = 0.0; est_out = 0.0;
+      return HMG_OK;
+    }
+    std::vector<cd> H((m + 1) * m), cs(m), sn(m), gv(m + 1), y(m);
+    auto Hs = [&](int i, int j) -> cd & { return H[(size_t)i * m + j]; };
+    double2 *dr = dres.template as<double2>();
+    bool have_res = false;
+    while (its < maxiter) {
+      if (!have_res) residual_d(s);                   // r = q - H x (fp64)
+      have_res = false;
+      const double beta = norm<double>(rd.template as<double2>(), s);
+      true_rel = beta / qn;
+      if (!std::isfinite(beta)) throw HmgError(HMG_EBREAKDOWN, "non-finite residual norm");
+      if (true_rel < tol) { converged = true; break; }
+      scale<double, T>(rd.template as<double2>(), Vp(0), 1.0 / beta, s);
+      std::fill(H.begin(), H.end(), cd(0, 0));
+      std::fill(gv.begin(), gv.end(), cd(0, 0));
+      gv[0] = beta;
+      int jend = 0;
+      bool stop = false;
+      for (int j = 0; j < m; ++j) {
+        cycle(0, Vp(j), Zp(j), 1, s);                // z_j = MG(v_j)
+        C *w = Vp(j + 1);
+        op(0, 0, Zp(j), nullptr, w, s);              // w = H z_j
+        const int nv = j + 1;
+        mdot<T, T>(V.template as<C>(), nv, w, dr, s);            // CGS pass 1
+        maxpy<T, T>(V.template as<C>(), nv, dr, -1.0, w, nullptr, s);
+        mdot<T, T>(V.template as<C>(), nv, w, dr + 32, s);       // CGS pass 2 (+ norm)
+        maxpy<T, T>(V.template as<C>(), nv, dr + 32, -1.0, w, dr + 64, s);
+        CK(cudaMemcpyAsync(hpin, dr, 65 * sizeof(double2), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const double2 *hh = reinterpret_cast<const double2 *>(hpin);
+        for (int i = 0; i <= j; ++i) Hs(i, j) = cd(hh[i].x + hh[32 + i].x, hh[i].y + hh[32 + i].y);
+        const double hn = std::sqrt(std::max(hh[64].x, 0.0));
+        for (int i = 0; i <= j; ++i)
+          if (!std::isfinite(Hs(i, j).real()) || !std::isfinite(Hs(i, j).imag()))
+            throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi coefficient");
+        if (!std::isfinite(hn)) throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi norm");
+        Hs(j + 1, j) = hn;
+        const bool breakdown = hn == 0.0;
+        if (!breakdown) scale<T, T>(w, w, 1.0 / hn, s);
+        for (int i = 0; i < j; ++i) {                // previous Givens rotations
+          const cd t = cs[i] * Hs(i, j) + sn[i] * Hs(i + 1, j);
+          Hs(i + 1, j) = -std::conj(sn[i]) * Hs(i, j) + std::conj(cs[i]) * Hs(i + 1, j);
+          Hs(i, j) = t;
+        }
+        const cd a = Hs(j, j), b = Hs(j + 1, j);
+        const double den = std::sqrt(std::norm(a) + std::norm(b));
+        if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; }
+        else if (std::abs(a) == 0.0) { cs[j] = 0.0; sn[j] = 1.0; }
+        else { cs[j] = std::abs(a) / den; sn[j] = (a / std::abs(a)) * std::conj(b) / den; }
+        Hs(j, j) = cs[j] * a + sn[j] * b;
+        Hs(j + 1, j) = 0.0;
+        gv[j + 1] = -std::conj(sn[j]) * gv[j];
+        gv[j] = cs[j] * gv[j];
+        ++its;
+        est = std::abs(gv[j + 1]) / qn;
+        hist.push_back(est);
+        jend = j + 1;
+        if (est < tol || breakdown || its >= maxiter) { stop = true; break; }
+      }
+      for (int i = jend - 1; i >= 0; --i) {           // back substitution
+        cd acc = gv[i];
+        for (int k = i + 1; k < jend; ++k) acc -= Hs(i, k) * y[k];
+        y[i] = acc / Hs(i, i);
+      }
+      double2 *yp = reinterpret_cast<double2 *>(hpin) + 128;
+      for (int i = 0; i < jend; ++i) yp[i] = make_double2(y[i].real(), y[i].imag());
+      CK(cudaMemcpyAsync(dr + 96, yp, jend * sizeof(double2), cudaMemcpyHostToDevice, s));
+      maxpy<T, double>(Z.template as<C>(), jend, dr + 96, 1.0, x, nullptr, s);   // x += Z y (fp64)
+      ++restarts;
+      residual_d(s);
+      have_res = true;
+      if (stop) {
+        true_rel = norm<double>(rd.template as<double2>(), s) / qn;
+        if (true_rel < tol) { converged = true; break; }
+      }
+    }
+    its_out = its;
+    restarts_out = restarts;
+    true_rel_out = true_rel;
+    est_out = est;
+    return converged ? HMG_OK : HMG_ENOTCONVERGED;
+  }
+
+  hmg_status api_fgmres(const void *q, void *x, int host, int m, double tol, int maxiter, cudaStream_t s,
+                        hmg_report *rep) override {
+    if (m < 1 || m >= KRY_MAXV) throw HmgError(HMG_EINVAL, "restart must be in [1, 31]");
+    if (!(tol > 0) || maxiter < 0) throw HmgError(HMG_EINVAL, "tol must be > 0 and maxiter >= 0");
+    ensure_ws(m, s);
+    const Geo &g = g0();
+    const int64_t N = g.nodes();
+    auto nl = node_launch(g);
+    const C *qsrc = (const C *)q;
+    if (host) {
+      CK(cudaMemcpyAsync(io.p, q, N * sizeof(C), cudaMemcpyHostToDevice, s));
+      qsrc = io.template as<C>();
+    }
+    tag("pack", 0, (double)(sizeof(C) + sizeof(double2)) * N);
+    launch(k_pack_cvt<T, double>, nl.grid, nl.block, 0, s, g, qsrc, 0, qd.template as<double2>(), 1);
+    CK(cudaEventRecord(ev0, s));
+    std::vector<double> hist;
+    int its = 0, restarts = 0;
+    double tr = 0, est = 0;
+    hmg_status st = fgmres(m, tol, maxiter, s, hist, its, restarts, tr, est);
+    CK(cudaEventRecord(ev1, s));
+    C *xdst = host ? io.template as<C>() : (C *)x;
+    tag("unpack", 0, (double)(sizeof(C) + sizeof(double2)) * N);
+    launch(k_pack_cvt<double, T>, nl.grid, nl.block, 0, s, g, (const double2 *)xd.template as<double2>(), 1, xdst, 0);
+    if (host) CK(cudaMemcpyAsync(x, io.p, N * sizeof(C), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (rep) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev0, ev1));
+      rep->iterations = its;
+      rep->converged = st == HMG_OK;
+      rep->restarts = restarts;
+      rep->relres_true = tr;
+      rep->relres_est = est;
+      rep->seconds = ms * 1e-3;
+      const int n = (int)hist.size();
+      rep->history_len = rep->history ? std::min(n, rep->history_cap) : 0;
+      for (int i = 0; i < rep->history_len; ++i) rep->history[i] = hist[i];
+      // c_f of Eq. 5.1 after a 5-iteration warm-up
+      const int wu = 5;
+      if (n > wu + 1) rep->c_f = std::pow(hist[n - 1] / hist[wu], 1.0 / (n - 1 - wu));
+      else rep->c_f = std::nan("");
+    }
+    return st;
+  }
+
+  // ------------------------------------------------------------ introspection
+  int64_t level_nodes(int l, int64_t n[3]) const override {
+    if (l < 0 || l >= L) return -1;
+    const Geo &g = lev[l].geo;
+    if (n) { n[0] = g.n[0]; n[1] = g.n[1]; n[2] = g.n[2]; }
+    return g.nodes();
+  }
+  int radius(int l) const override { return (l < 0 || l >= L) ? -1 : lev[l].r; }
+  int copy_stencil(int l, double *out, int64_t cap) override {
+    check_level(l);
+    cudaStream_t s = 0;
+    const Geo &g = lev[l].geo;
+    const int K = kcount(opt.dim, lev[l].r);
+    const int64_t N = g.nodes();
+    if (cap < (int64_t)K * N * 2) throw HmgError(HMG_EINVAL, "output buffer too small");
+    DBuf tmp, dst;
+    dst.alloc((size_t)K * N * sizeof(double2), s);
+    auto nl = node_launch(g);
+    if (l == 0) {
+      materialize(g, lev[0].h, w2k2.template as<double>(), gq.template as<double>(), tmp, s);
+      launch(k_compact_stencil<double>, nl.grid, nl.block, 0, s, g, K, (const double2 *)tmp.template as<double2>(), dst.template as<double2>());
+    } else {
+      launch(k_compact_stencil<T>, nl.grid, nl.block, 0, s, g, K, (const C *)lev[l].coef.template as<C>(), dst.template as<double2>());
+    }
+    CK(cudaMemcpy(out, dst.p, (size_t)K * N * sizeof(double2), cudaMemcpyDeviceToHost));
+    return K;
+  }
+};
+
+}  // namespace hmg
+
+// =====================================================================  C-ABI
+struct hmg_hierarchy {
+  std::unique_ptr<hmg::SolverBase> impl;
+};
+
+static thread_local std::string t_err;
+
+static hmg_status fail(hmg_status s, const std::string &m) {
+  t_err = m;
+  return s;
+}
+
+#define HMG_API_BEGIN try {
+#define HMG_API_END                                                 \
+  }                                                                 \
+  catch (const hmg::HmgError &e) { return fail(e.st, e.what()); }   \
+  catch (const std::bad_alloc &) { return fail(HMG_ENOMEM, "host allocation failed"); } \
+  catch (const std::exception &e) { return fail(HMG_ECUDA, e.what()); }
+
+static cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+hmg_status hmg_build_hierarchy(const hmg_options *o, const double *kappa, double omega, const double *gamma,
+                               double alpha, void *stream, hmg_hierarchy **out) {
+  HMG_API_BEGIN
+  if (!o || !kappa || !gamma || !out) return fail(HMG_EINVAL, "null pointer");
+  *out = nullptr;
+  if (o->dim != 2 && o->dim != 3) return fail(HMG_EINVAL, "dim must be 2 or 3");
+  if (o->levels < 2 || o->levels > 16) return fail(HMG_EINVAL, "levels must be in [2, 16]");
+  if (!(o->h > 0)) return fail(HMG_EINVAL, "h must be > 0");
+  if (!(omega > 0)) return fail(HMG_EINVAL, "omega must be > 0");
+  if (!(alpha >= 0)) return fail(HMG_EINVAL, "shift alpha must be >= 0");
+  if (o->nu1 < 0 || o->nu2 < 0 || o->cycle < 0 || o->cycle > 1) return fail(HMG_EINVAL, "bad nu1/nu2/cycle");
+  if (o->fine_stencil != HMG_COMPACT4 && o->fine_stencil != HMG_FD2) return fail(HMG_EINVAL, "bad fine_stencil");
+  if (o->coarse_op != HMG_GALERKIN && o->coarse_op != HMG_REDISCRETIZE) return fail(HMG_EINVAL, "bad coarse_op");
+  if (o->smoother < 0 || o->smoother > 3) return fail(HMG_EINVAL, "bad smoother");
+  if (o->smoother == HMG_VANKA_RB && o->dim != 2)
+    return fail(HMG_EINVAL, "RB patch is 2D only (the 13-node 3D RB patch is rejected by the paper, P:949-951)");
+  if (o->dtype != HMG_C64 && o->dtype != HMG_C128) return fail(HMG_EINVAL, "bad dtype");
+  if (!o->damping || o->n_damping < 1) return fail(HMG_EINVAL, "damping required");
+  int64_t N = 1;
+  for (int a = 0; a < o->dim; ++a) {
+    const int64_t c = o->cells[a];
+    if (c < 4 || c % (1LL << (o->levels - 1)) != 0)
+      return fail(HMG_EINVAL, "cells must be >= 4 and divisible by 2^(levels-1)");
+    N *= c + 1;
+  }
+  for (int64_t i = 0; i < N; ++i) {
+    if (!(kappa[i] > 0) || !std::isfinite(kappa[i])) return fail(HMG_EINVAL, "kappa must be finite and > 0");
+    if (!(gamma[i] >= 0) || !std::isfinite(gamma[i])) return fail(HMG_EINVAL, "gamma must be finite and >= 0");
+  }
+  std::unique_ptr<hmg_hierarchy> h(new hmg_hierarchy);
+  if (o->dtype == HMG_C64) h->impl.reset(new hmg::Solver<float>);
+  else h->impl.reset(new hmg::Solver<double>);
+  h->impl->opt = *o;
+  h->impl->damping.assign(o->damping, o->damping + o->n_damping);
+  h->impl->opt.damping = nullptr;
+  h->impl->build(kappa, omega, gamma, alpha, S(stream));
+  *out = h.release();
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_apply_helmholtz(const hmg_hierarchy *h, int level, int shifted, const void *x, void *y, void *stream) {
+  HMG_API_BEGIN
+  if (!h || !x || !y) return fail(HMG_EINVAL, "null pointer");
+  h->impl->api_apply(level, shifted, x, y, S(stream));
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_residual(const hmg_hierarchy *h, int level, int shifted, const void *f, const void *x, void *r,
+                        void *stream) {
+  HMG_API_BEGIN
+  if (!h || !f || !x || !r) return fail(HMG_EINVAL, "null pointer");
+  h->impl->api_residual(level, shifted, f, x, r, S(stream));
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_smooth(const hmg_hierarchy *h, int level, const void *f, void *u, void *stream) {
+  HMG_API_BEGIN
+  if (!h || !f || !u) return fail(HMG_EINVAL, "null pointer");
+  h->impl->api_smooth(level, f, u, S(stream));
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_restrict(const hmg_hierarchy *h, int level, const void *r, void *fc, void *stream) {
+  HMG_API_BEGIN
+  if (!h || !r || !fc) return fail(HMG_EINVAL, "null pointer");
+  h->impl->api_restrict(level, r, fc, S(stream));
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_prolong_add(const hmg_hierarchy *h, int level, const void *ec, void *u, void *stream) {
+  HMG_API_BEGIN
+  if (!h || !ec || !u) return fail(HMG_EINVAL, "null pointer");
+  h->impl->api_prolong(level, ec, u, S(stream));
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_coarse_solve(const hmg_hierarchy *h, const void *r, void *e, void *stream) {
+  HMG_API_BEGIN
+  if (!h || !r || !e) return fail(HMG_EINVAL, "null pointer");
+  h->impl->api_coarse(r, e, S(stream));
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_vcycle(const hmg_hierarchy *h, const void *f, void *x, int x_is_zero, void *stream) {
+  HMG_API_BEGIN
+  if (!h || !f || !x) return fail(HMG_EINVAL, "null pointer");
+  h->impl->api_vcycle(f, x, x_is_zero, S(stream));
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_fgmres_solve(const hmg_hierarchy *h, const void *q, void *x, int restart, double tol, int maxiter,
+                            void *stream, hmg_report *rep) {
+  HMG_API_BEGIN
+  if (!h || !q || !x) return fail(HMG_EINVAL, "null pointer");
+  hmg_status st = h->impl->api_fgmres(q, x, 0, restart, tol, maxiter, S(stream), rep);
+  if (st == HMG_ENOTCONVERGED) t_err = "FGMRES reached maxiter without converging";
+  return st;
+  HMG_API_END
+}
+
+hmg_status hmg_fgmres_solve_host(const hmg_hierarchy *h, const void *q, void *x, int restart, double tol,
+                                 int maxiter, void *stream, hmg_report *rep) {
+  HMG_API_BEGIN
+  if (!h || !q || !x) return fail(HMG_EINVAL, "null pointer");
+  hmg_status st = h->impl->api_fgmres(q, x, 1, restart, tol, maxiter, S(stream), rep);
+  if (st == HMG_ENOTCONVERGED) t_err = "FGMRES reached maxiter without converging";
+  return st;
+  HMG_API_END
+}
+
+int hmg_num_levels(const hmg_hierarchy *h) { return h ? h->impl->L : -1; }
+
+int64_t hmg_level_nodes(const hmg_hierarchy *h, int level, int64_t n[3]) {
+  return h ? h->impl->level_nodes(level, n) : -1;
+}
+
+int hmg_stencil_radius(const hmg_hierarchy *h, int level) { return h ? h->impl->radius(level) : -1; }
+
+int hmg_copy_stencil(const hmg_hierarchy *h, int level, double *out, int64_t cap) {
+  try {
+    if (!h || !out) { t_err = "null pointer"; return -1; }
+    return h->impl->copy_stencil(level, out, cap);
+  } catch (const std::exception &e) {
+    t_err = e.what();
+    return -1;
+  }
+}
+
+int64_t hmg_launch_count(void) { return hmg::g_launches.load(); }
+
+void hmg_profile_begin(void) {
+  hmg::g_prof.recs.clear();
+  hmg::g_prof.used = 0;
+  hmg::g_prof.on = true;
+}
+
+const char *hmg_profile_report(void) {
+  static thread_local std::string out;
+  hmg::g_prof.on = false;
+  struct Agg { long long n = 0; double ms = 0, bytes = 0; };
+  std::vector<std::pair<std::string, Agg>> agg;
+  for (auto &r : hmg::g_prof.recs) {
+    float ms = 0;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) ms = 0;
+    auto it = std::find_if(agg.begin(), agg.end(), [&](const std::pair<std::string, Agg> &p) { return p.first == r.name; });
+    if (it == agg.end()) { agg.push_back({r.name, Agg{}}); it = agg.end() - 1; }
+    it->second.n += 1;
+    it->second.ms += ms;
+    it->second.bytes += r.bytes;
+  }
+  out = "{";
+  for (size_t i = 0; i < agg.size(); ++i) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "%s\"%s\": {\"launches\": %lld, \"ms\": %.6f, \"bytes\": %.0f}", i ? ", " : "",
+             agg[i].first.c_str(), agg[i].second.n, agg[i].second.ms, agg[i].second.bytes);
+    out += buf;
+  }
+  out += "}";
+  hmg::g_prof.recs.clear();
+  hmg::g_prof.used = 0;
+  return out.c_str();
+}
+
+void hmg_hierarchy_destroy(hmg_hierarchy *h) { delete h; }
+
+const char *hmg_last_error(void) { return t_err.c_str(); }
+
+const char *hmg_version(void) { return "hmg 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// k_operator.cuh -- fine-level matrix-free Helmholtz stencil (SURVEY §8(a) a2,
+// a11) and stored-coefficient stencil of the Galerkin levels (a6).
+//
+//   H = L - diag(sigma) M   (Eq. 2.2; Eq. 2.3)
+//   2D COMPACT4: L = (1/h^2)[-1/6 -2/3 -1/6; -2/3 10/3 -2/3; -1/6 -2/3 -1/6],
+//                M = [0 1/12 0; 1/12 2/3 1/12; 0 1/12 0]
+//   3D COMPACT4: L = -1/(6h^2){[0 1 0;1 2 1;0 1 0], [1 2 1;2 -24 2;1 2 1], [0 1 0;1 2 1;0 1 0]}
+//                i.e. centre 4/h^2, 6 faces -1/(3h^2), 12 edges -1/(6h^2), corners 0;
+//                M = centre 1/2, faces 1/12.
+//   FD2: L = (1/h^2)(2d centre, -1 on the 2d faces), M = I.
+// sigma multiplies row j (the row's centre node); the shifted operator uses
+// sigma_s = sigma - i alpha Re(sigma)  (= w^2k^2 (1 - i(g/w + alpha)),
+// readings A1/A2 of P:247-253).  Out-of-domain neighbours are the zero ghost
+// layer of the padded box (truncation = homogeneous Dirichlet).
+#pragma once
+#include "common.cuh"
+
+namespace hmg {
+
+enum { ST_COMPACT4 = 0, ST_FD2 = 1 };
+
+// Stencil weights of L (without 1/h^2) and M by neighbour class.
+template <int DIM, int KIND> struct FineW;
+template <> struct FineW<2, ST_COMPACT4> {
+  static constexpr double Lc = 10.0 / 3.0, Lf = -2.0 / 3.0, Le = -1.0 / 6.0;
+  static constexpr double Mc = 2.0 / 3.0, Mf = 1.0 / 12.0;
+};
+template <> struct FineW<3, ST_COMPACT4> {
+  static constexpr double Lc = 4.0, Lf = -1.0 / 3.0, Le = -1.0 / 6.0;
+  static constexpr double Mc = 0.5, Mf = 1.0 / 12.0;
+};
+template <> struct FineW<2, ST_FD2> {
+  static constexpr double Lc = 4.0, Lf = -1.0, Le = 0.0;
+  static constexpr double Mc = 1.0, Mf = 0.0;
+};
+template <> struct FineW<3, ST_FD2> {
+  static constexpr double Lc = 6.0, Lf = -1.0, Le = 0.0;
+  static constexpr double Mc = 1.0, Mf = 0.0;
+};
+
+// y = A x   (f == nullptr)   or   y = f - A x   (residual), fine level.
+// sig[j] = sigma_j = (w^2k^2, -w^2k^2 g/w); alpha = shift (0 for H).
+template <typename T, int DIM, int KIND>
+__global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<T> *__restrict__ sig, T alpha, T ih2,
+                                                 const cplx<T> *__restrict__ x,
+                                                 const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y) {
+  HMG_NODE_IDX(g, ix, iy, iz);
+  using W = FineW<DIM, KIND>;
+  const int64_t i = g.idx(ix, iy, iz);
+  const int64_t px = g.px;
+  const cplx<T> xc = x[i];
+  cplx<T> sf = cadd<T>(cadd<T>(x[i - 1], x[i + 1]), cadd<T>(x[i - px], x[i + px]));
+  cplx<T> se = mkc<T>(0, 0);
+  if (DIM == 2) {
+    if (W::Le != 0.0) se = cadd<T>(cadd<T>(x[i - px - 1], x[i - px + 1]), cadd<T>(x[i + px - 1], x[i + px + 1]));
+  } else {
+    const int64_t pz = g.pxy;
+    sf = cadd<T>(sf, cadd<T>(x[i - pz], x[i + pz]));
+    if (W::Le != 0.0) {
+      se = cadd<T>(cadd<T>(x[i - px - 1], x[i - px + 1]), cadd<T>(x[i + px - 1], x[i + px + 1]));
+      se = cadd<T>(se, cadd<T>(cadd<T>(x[i - pz - 1], x[i - pz + 1]), cadd<T>(x[i + pz - 1], x[i + pz + 1])));
+      se = cadd<T>(se, cadd<T>(cadd<T>(x[i - pz - px], x[i - pz + px]), cadd<T>(x[i + pz - px], x[i + pz + px])));
+    }
+  }
+  // L x
+  cplx<T> Lx = cscale<T>(xc, (T)W::Lc);
+  Lx = cfmar<T>(Lx, (T)W::Lf, sf);
+  if (W::Le != 0.0) Lx = cfmar<T>(Lx, (T)W::Le, se);
+  Lx = cscale<T>(Lx, ih2);
+  // M x
+  cplx<T> Mx = cscale<T>(xc, (T)W::Mc);
+  if (W::Mf != 0.0) Mx = cfmar<T>(Mx, (T)W::Mf, sf);
+  cplx<T> s = sig[i];
+  s.y = fma(-alpha, s.x, s.y);
+  cplx<T> Ax = csub<T>(Lx, cmul<T>(s, Mx));
+  y[i] = f ? csub<T>(f[i], Ax) : Ax;
+}
+
+// Stored stencil of radius R: coef[k][j], k = (ox+R) + (2R+1)((oy+R) + (2R+1)(oz+R)),
+// multiplies x[j + o].  Coefficients towards out-of-domain nodes are zero.
+template <typename T, int DIM, int R>
+__global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<T> *__restrict__ coef,
+                                                   const cplx<T> *__restrict__ x,
+                                                   const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y) {
+  HMG_NODE_IDX(g, ix, iy, iz);
+  const int64_t i = g.idx(ix, iy, iz);
+  constexpr int W = 2 * R + 1;
+  constexpr int ZR = DIM == 3 ? R : 0;
+  cplx<T> acc = mkc<T>(0, 0);
+  int k = 0;
+#pragma unroll
+  for (int oz = -ZR; oz <= ZR; ++oz)
+#pragma unroll
+    for (int oy = -R; oy <= R; ++oy)
+#pragma unroll
+      for (int ox = -R; ox <= R; ++ox, ++k) {
+        const cplx<T> c = coef[(int64_t)k * g.total + i];
+        acc = cfma<T>(acc, c, x[i + g.delta(ox, oy, oz)]);
+      }
+  (void)W;
+  y[i] = f ? csub<T>(f[i], acc) : acc;
+}
+
+}  // namespace hmg

@@ -1,0 +1,95 @@
+// k_transfer.cuh -- intergrid transfers (§3.1).
+//
+// 1D restriction weights centred at fine node 2I (coarse node I == fine 2I):
+//   lin [1 2 1]/4        (Eq. 3.1; full weighting)
+//   cub [1 4 6 4 1]/16   (Eq. 3.2; bicubic)
+// dD operators are tensor products (Eqs. 3.5-3.6); P = 2^d R^T of
+// the P-kind weights, i.e. per axis: even fine node 2J gets
+// (1/8, 3/4, 1/8) of coarse (J-1, J, J+1) for cub and 1 x J for lin; odd fine
+// node 2J+1 gets 1/2 of J and 1/2 of J+1 for both.  Truncation at the boundary
+// comes from the zero ghost layer (reading A5).
+#pragma once
+#include "common.cuh"
+
+namespace hmg {
+
+template <int RR> struct RW;
+template <> struct RW<1> {
+  __device__ static constexpr double w(int k) { return k == 0 ? 0.5 : 0.25; }
+};
+template <> struct RW<2> {
+  __device__ static constexpr double w(int k) { return k == 0 ? 0.375 : (k == 1 || k == -1) ? 0.25 : 0.0625; }
+};
+
+// fc[I] = sum_k w(k) r[2I + k]     (coarse-node parallel)
+template <typename T, int DIM, int RR>
+__global__ void __launch_bounds__(256) k_restrict(Geo gf, Geo gc, const cplx<T> *__restrict__ r,
+                                                  cplx<T> *__restrict__ fc) {
+  HMG_NODE_IDX(gc, X, Y, Z);
+  const int64_t ic = gc.idx(X, Y, Z);
+  const int64_t jf = gf.idx(2 * X, 2 * Y, DIM == 3 ? 2 * Z : 0);
+  constexpr int ZR = DIM == 3 ? RR : 0;
+  cplx<T> acc = mkc<T>(0, 0);
+#pragma unroll
+  for (int kz = -ZR; kz <= ZR; ++kz) {
+    cplx<T> accy = mkc<T>(0, 0);
+#pragma unroll
+    for (int ky = -RR; ky <= RR; ++ky) {
+      cplx<T> accx = mkc<T>(0, 0);
+#pragma unroll
+      for (int kx = -RR; kx <= RR; ++kx) accx = cfmar<T>(accx, (T)RW<RR>::w(kx), r[jf + gf.delta(kx, ky, kz)]);
+      accy = cfmar<T>(accy, (T)RW<RR>::w(ky), accx);
+    }
+    acc = DIM == 3 ? cfmar<T>(acc, (T)RW<RR>::w(kz), accy) : accy;
+  }
+  fc[ic] = acc;
+}
+
+// u[i] += sum_J P[i, J] e[J]     (fine-node parallel)
+template <int PR>
+__device__ __forceinline__ int prolong_taps(int i, int *J, double *w) {
+  // returns number of taps along one axis for fine coordinate i
+  if ((i & 1) == 0) {
+    const int c = i >> 1;
+    if (PR == 2) {
+      J[0] = c - 1; w[0] = 0.125;
+      J[1] = c;     w[1] = 0.75;
+      J[2] = c + 1; w[2] = 0.125;
+      return 3;
+    }
+    J[0] = c; w[0] = 1.0;
+    return 1;
+  }
+  const int c = (i - 1) >> 1;
+  J[0] = c;     w[0] = 0.5;
+  J[1] = c + 1; w[1] = 0.5;
+  return 2;
+}
+
+template <typename T, int DIM, int PR>
+__global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<T> *__restrict__ e,
+                                                     cplx<T> *__restrict__ u) {
+  HMG_NODE_IDX(gf, ix, iy, iz);
+  int Jx[3], Jy[3], Jz[3];
+  double wx[3], wy[3], wz[3];
+  const int nx = prolong_taps<PR>(ix, Jx, wx);
+  const int ny = prolong_taps<PR>(iy, Jy, wy);
+  int nz = 1;
+  Jz[0] = 0; wz[0] = 1.0;
+  if (DIM == 3) nz = prolong_taps<PR>(iz, Jz, wz);
+  cplx<T> acc = mkc<T>(0, 0);
+  for (int c = 0; c < nz; ++c) {
+    cplx<T> accy = mkc<T>(0, 0);
+    for (int b = 0; b < ny; ++b) {
+      cplx<T> accx = mkc<T>(0, 0);
+      const int64_t row = gc.base + (int64_t)Jz[c] * gc.pxy + (int64_t)Jy[b] * gc.px;
+      for (int a = 0; a < nx; ++a) accx = cfmar<T>(accx, (T)wx[a], e[row + Jx[a]]);
+      accy = cfmar<T>(accy, (T)wy[b], accx);
+    }
+    acc = cfmar<T>(acc, (T)wz[c], accy);
+  }
+  const int64_t i = gf.idx(ix, iy, iz);
+  u[i] = cadd<T>(u[i], acc);
+}
+
+}  // namespace hmg

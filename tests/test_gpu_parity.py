@@ -1,0 +1,331 @@
+"""Parity of the CUDA path (libhmg.so through its C-ABI) against the CPU oracle.
+
+Tolerances (north_star in BASELINE.json):
+  single operator applications  c128 <= 1e-12, c64 <= 1e-5   (max-abs relative)
+  Galerkin stencils, transfers, one smoothing step, coarse solve: same bar
+  one V-cycle: c128 <= 1e-10 (composition of ~10 operators and the coarsest
+  dense inverse, whose condition number amplifies rounding), c64 <= 1e-4
+  FGMRES: iterations within +-1 (c128) / +-2 (c64), true relres <= tol.
+"""
+import numpy as np
+import pytest
+
+from helpers import build_pair, problem, rel_err, stencil_from_sparse, to_dev, to_host
+from paper_2511_16808_b200 import media
+
+pytestmark = pytest.mark.gpu
+
+TOL_OP = {"c128": 1e-12, "c64": 1e-5}
+TOL_CYCLE = {"c128": 1e-10, "c64": 1e-4}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2511_16808_b200.hmg  # noqa: F401  (fails loudly if libhmg.so is missing)
+
+
+def _rand(n, seed):
+    return media.random_complex(n, seed)
+
+
+# ------------------------------------------------------------------ a2 / a11
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("stencil", ["compact4", "fd2"])
+@pytest.mark.parametrize("dim,cells", [(2, (40, 24)), (3, (12, 8, 16))])
+def test_apply_fine(dim, cells, stencil, dtype):
+    p = problem(dim, cells)
+    gh, oh = build_pair(p, levels=2, fine_stencil=stencil, dtype=dtype,
+                        smoother="jacobi")
+    x = _rand(oh.A[0].shape[0], 1)
+    for shifted, A in ((False, oh.H), (True, oh.A[0])):
+        xd = to_dev(x, dtype)
+        yd = xd.clone()
+        gh.apply_helmholtz(xd, yd, level=0, shifted=shifted)
+        assert rel_err(to_host(yd), A @ x) <= TOL_OP[dtype]
+        fd = to_dev(_rand(x.size, 2), dtype)
+        rd = xd.clone()
+        gh.residual(fd, xd, rd, level=0, shifted=shifted)
+        f = to_host(fd)
+        xx = to_host(xd)
+        assert rel_err(to_host(rd), f - A @ xx) <= TOL_OP[dtype]
+
+
+def test_apply_fine_full_size_sampled():
+    """BASELINE config 1 at N=4096 (c64, the bench workload): sampled rows of
+    H x computed one by one from the paper's stencil weights."""
+    import torch
+    N = 4096
+    p = media.config_problem(1, n=N)
+    from paper_2511_16808_b200 import hmg
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=9, damping=[0.83, 0.5, 0.4, 0.65], dtype="c64")
+    gh = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.25)
+    n = N + 1
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(n * n, dtype=torch.complex64, generator=g)
+    y = torch.empty_like(x).cuda()
+    gh.apply_helmholtz(x.cuda(), y, level=0, shifted=False)
+    y = y.cpu().numpy()
+    xs = x.numpy().astype(np.complex128).reshape(n, n)
+    rng = np.random.default_rng(0)
+    pts = [(0, 0), (n - 1, n - 1), (0, n // 2), (n // 2, n // 2)] + [tuple(rng.integers(0, n, 2)) for _ in range(400)]
+    h = p.h
+    k2 = (p.kappa ** 2 * p.omega ** 2)
+    sig = k2 * (1 - 1j * p.gamma / p.omega)
+    L = {0: 10 / 3, 1: -2 / 3, 2: -1 / 6}
+    M = {0: 2 / 3, 1: 1 / 12, 2: 0.0}
+    for (iy, ix) in pts:
+        acc, scale = 0, 0
+        for oy in (-1, 0, 1):
+            for ox in (-1, 0, 1):
+                jy, jx = iy + oy, ix + ox
+                if 0 <= jy < n and 0 <= jx < n:
+                    c = abs(ox) + abs(oy)
+                    term = (L[c] / h ** 2 - sig[iy, ix] * M[c]) * xs[jy, jx]
+                    acc += term
+                    scale += abs(term)
+        # fp32 rounding bound of a 9-term complex sum, relative to sum |terms|
+        assert abs(y[iy * n + ix] - acc) <= 1e-5 * scale
+
+
+# ------------------------------------------------------------------ a6 / a7
+@pytest.mark.parametrize("dim,cells,levels,intergrid,coarse_op", [
+    (2, (32, 24), 3, "levdep", "galerkin"),
+    (2, (32, 16), 3, "linear", "galerkin"),
+    (2, (32, 16), 3, "mixed", "galerkin"),
+    (2, (32, 16), 3, "cubic", "galerkin"),
+    (2, (32, 16), 3, "levdep", "rediscretize"),
+    (3, (8, 8, 16), 3, "levdep", "galerkin"),
+    (3, (8, 16, 8), 3, "linear", "galerkin"),
+])
+def test_coarse_stencils(dim, cells, levels, intergrid, coarse_op):
+    p = problem(dim, cells)
+    gh, oh = build_pair(p, levels=levels, intergrid=intergrid, coarse_op=coarse_op,
+                        smoother="jacobi")
+    for l in range(levels):
+        got = gh.copy_stencil(l)
+        r = gh.stencil_radius(l)
+        want = stencil_from_sparse(oh.A[l], oh.nodes[l], r)
+        assert got.shape == want.shape
+        assert rel_err(got, want) <= 1e-12, f"level {l}"
+
+
+# ------------------------------------------------------------------ a3 / a5
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("dim,cells,intergrid", [(2, (48, 32), "levdep"), (2, (32, 32), "linear"),
+                                                 (3, (16, 8, 8), "levdep")])
+def test_transfers(dim, cells, intergrid, dtype):
+    p = problem(dim, cells)
+    gh, oh = build_pair(p, levels=3, intergrid=intergrid, dtype=dtype, smoother="jacobi")
+    for l in range(2):
+        r = _rand(oh.A[l].shape[0], 10 + l)
+        fc = to_dev(np.zeros(oh.A[l + 1].shape[0]), dtype)
+        rd = to_dev(r, dtype)
+        gh.restrict(rd, fc, level=l)
+        assert rel_err(to_host(fc), oh.R[l] @ to_host(rd)) <= TOL_OP[dtype]
+        e = to_dev(_rand(oh.A[l + 1].shape[0], 20 + l), dtype)
+        u = to_dev(_rand(oh.A[l].shape[0], 30 + l), dtype)
+        u0 = to_host(u)
+        gh.prolong_add(e, u, level=l)
+        assert rel_err(to_host(u), u0 + oh.P[l] @ to_host(e)) <= TOL_OP[dtype]
+
+
+# ------------------------------------------------------------------ a4
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("dim,cells,smoother", [
+    (2, (24, 16), "rb"), (2, (16, 24), "element"), (2, (16, 16), "plus"), (2, (16, 16), "jacobi"),
+    (3, (8, 8, 16), "element"), (3, (8, 8, 8), "plus"), (3, (8, 16, 8), "jacobi"),
+])
+def test_smooth(dim, cells, smoother, dtype):
+    p = problem(dim, cells)
+    gh, oh = build_pair(p, levels=3, smoother=smoother, dtype=dtype)
+    from oracle.cycle import smooth
+    for l in range(2):
+        n = oh.A[l].shape[0]
+        f = to_dev(_rand(n, 40 + l), dtype)
+        u = to_dev(_rand(n, 50 + l), dtype)
+        fh, uh = to_host(f), to_host(u)
+        gh.smooth(f, u, level=l)
+        want = smooth(oh, l, fh, uh)
+        tol = TOL_OP[dtype] * (10 if dtype == "c128" else 1)
+        assert rel_err(to_host(u), want) <= tol, f"level {l}"
+
+
+def test_fd2_rb_is_jacobi():
+    """under FD2 the RB patch has no couplings, so the RB
+    smoother equals damped Jacobi with the same damping."""
+    p = problem(2, (16, 16))
+    g1, _ = build_pair(p, levels=2, smoother="rb", fine_stencil="fd2", oracle=False)
+    from paper_2511_16808_b200 import hmg
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=2, smoother="jacobi", fine_stencil="fd2",
+                       damping=[0.83, 0.5])
+    g2 = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.3)
+    n = 17 * 17
+    f = to_dev(_rand(n, 1))
+    u1 = to_dev(_rand(n, 2))
+    u2 = u1.clone()
+    g1.smooth(f, u1)
+    g2.smooth(f, u2)
+    assert rel_err(to_host(u1), to_host(u2)) <= 1e-13
+
+
+# ------------------------------------------------------------------ a8
+@pytest.mark.parametrize("dim,cells", [(2, (32, 16)), (3, (8, 8, 8))])
+def test_coarse_solve(dim, cells):
+    p = problem(dim, cells)
+    gh, oh = build_pair(p, levels=3, smoother="jacobi")
+    from oracle.hierarchy import coarse_solve
+    n = oh.A[-1].shape[0]
+    r = _rand(n, 7)
+    e = to_dev(np.zeros(n))
+    gh.coarse_solve(to_dev(r), e)
+    assert rel_err(to_host(e), coarse_solve(oh, r)) <= 1e-11
+    # residual of the direct solve
+    assert rel_err(oh.A[-1] @ to_host(e), r) <= 1e-11
+
+
+# ------------------------------------------------------------------ a9
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("dim,cells,levels,kw", [
+    (2, (64, 48), 4, {}),
+    (2, (32, 32), 3, {"cycle": "W"}),
+    (2, (32, 32), 3, {"nu1": 2, "nu2": 0}),
+    (2, (32, 32), 3, {"smoother": "jacobi", "intergrid": "linear"}),
+    (3, (16, 16, 8), 3, {}),
+])
+def test_vcycle(dim, cells, levels, kw, dtype):
+    p = problem(dim, cells)
+    gh, oh = build_pair(p, levels=levels, dtype=dtype, **kw)
+    from oracle.cycle import vcycle
+    n = oh.A[0].shape[0]
+    f = _rand(n, 60)
+    fd = to_dev(f, dtype)
+    x = to_dev(np.zeros(n), dtype)
+    gh.vcycle(fd, x, x_is_zero=True)
+    assert rel_err(to_host(x), vcycle(oh, to_host(fd))) <= TOL_CYCLE[dtype]
+    # nonzero initial guess
+    u0 = _rand(n, 61)
+    x = to_dev(u0, dtype)
+    gh.vcycle(fd, x, x_is_zero=False)
+    assert rel_err(to_host(x), vcycle(oh, to_host(fd), to_host(to_dev(u0, dtype)))) <= TOL_CYCLE[dtype]
+
+
+# ------------------------------------------------------------------ a10 end to end
+def _config0(dtype, smoother="rb", intergrid="levdep", alpha=0.15):
+    p = media.config_problem(0)
+    damping = [0.83, 0.5, 0.4, 0.65] if smoother == "rb" else [0.89, 0.9, 0.3, 0.71]
+    from paper_2511_16808_b200 import hmg
+    from oracle.hierarchy import Options as OOptions, build_hierarchy
+    from oracle.fgmres import fgmres_solve
+    from oracle.cycle import vcycle
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=4, smoother=smoother, intergrid=intergrid,
+                       damping=damping, dtype=dtype)
+    gh = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, alpha)
+    oo = OOptions(dim=2, cells=p.cells, h=p.h, levels=4, smoother=smoother, intergrid=intergrid, damping=damping)
+    oh = build_hierarchy(oo, p.kappa, p.omega, p.gamma, alpha)
+    xo, info = fgmres_solve(oh.H, p.q.ravel(), lambda v: vcycle(oh, v), restart=10, tol=1e-6, maxiter=500)
+    return p, gh, xo, info
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_fgmres_config0(dtype):
+    p, gh, xo, info = _config0(dtype)
+    import torch
+    q = to_dev(p.q, dtype)
+    x = torch.zeros_like(q)
+    rep = gh.fgmres_solve(q, x, restart=10, tol=1e-6, maxiter=500)
+    assert rep.converged and rep.relres_true <= 1e-6
+    slack = 1 if dtype == "c128" else 2
+    assert abs(rep.iterations - info["iterations"]) <= slack, (rep.iterations, info["iterations"])
+    assert rel_err(to_host(x), xo) <= (1e-5 if dtype == "c128" else 1e-3)
+    # residual history matches iteration by iteration while well above rounding
+    h = np.array(rep.history)
+    ho = np.array(info["history"])
+    m = min(len(h), len(ho), 20)
+    assert np.allclose(h[:m], ho[:m], rtol=1e-6 if dtype == "c128" else 1e-2)
+
+
+def test_fgmres_config0_plain_cslp():
+    """Plain CSLP comparison of config 0: Jacobi + LINEAR intergrid, alpha 0.5."""
+    p, gh, xo, info = _config0("c128", smoother="jacobi", intergrid="linear", alpha=0.5)
+    import torch
+    q = to_dev(p.q)
+    x = torch.zeros_like(q)
+    rep = gh.fgmres_solve(q, x, restart=10, tol=1e-6, maxiter=500)
+    assert rep.converged and abs(rep.iterations - info["iterations"]) <= 1
+
+
+def test_fgmres_host_entry_matches_device():
+    p = media.config_problem(0)
+    from paper_2511_16808_b200 import hmg
+    import torch
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=4, dtype="c128")
+    gh = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.15)
+    q = to_dev(p.q)
+    x = torch.zeros_like(q)
+    r1 = gh.fgmres_solve(q, x, restart=10)
+    qh = q.cpu().pin_memory()
+    xh = torch.zeros_like(qh).pin_memory()
+    r2 = gh.fgmres_solve_host(qh, xh, restart=10)
+    assert r1.iterations == r2.iterations
+    assert torch.equal(x.cpu(), xh)
+
+
+def test_fgmres_3d_small():
+    p = problem(3, (16, 16, 16), sponge=4, hetero=False)
+    gh, oh = build_pair(p, levels=3, alpha=0.5)
+    from oracle.fgmres import fgmres_solve
+    from oracle.cycle import vcycle
+    import torch
+    xo, info = fgmres_solve(oh.H, p.q.ravel(), lambda v: vcycle(oh, v), restart=10, tol=1e-6, maxiter=300)
+    q = to_dev(p.q)
+    x = torch.zeros_like(q)
+    rep = gh.fgmres_solve(q, x, restart=10, tol=1e-6, maxiter=300)
+    assert rep.converged and abs(rep.iterations - info["iterations"]) <= 1
+
+
+# ------------------------------------------------------------------ edge cases / errors
+def test_minimum_grid():
+    p = problem(2, (4, 4))
+    gh, oh = build_pair(p, levels=2)
+    from oracle.cycle import vcycle
+    f = _rand(25, 3)
+    x = to_dev(np.zeros(25))
+    gh.vcycle(to_dev(f), x)
+    assert rel_err(to_host(x), vcycle(oh, f)) <= 1e-10
+
+
+def test_zero_rhs():
+    p = problem(2, (16, 16))
+    gh, _ = build_pair(p, levels=3, oracle=False)
+    import torch
+    q = torch.zeros(17 * 17, dtype=torch.complex128, device="cuda")
+    x = torch.ones_like(q)
+    rep = gh.fgmres_solve(q, x)
+    assert rep.converged and rep.iterations == 0 and torch.count_nonzero(x) == 0
+
+
+def test_errors():
+    from paper_2511_16808_b200 import hmg
+    p = problem(2, (16, 16))
+    with pytest.raises(hmg.HmgError) as e:
+        hmg.Hierarchy(hmg.Options(dim=2, cells=(18, 16), h=p.h, levels=3), np.ones(19 * 17), p.omega,
+                      np.zeros(19 * 17), 0.1)
+    assert e.value.status == hmg.EINVAL
+    bad = p.kappa.copy()
+    bad.flat[5] = -1
+    with pytest.raises(hmg.HmgError) as e:
+        hmg.Hierarchy(hmg.Options(dim=2, cells=p.cells, h=p.h, levels=3), bad, p.omega, p.gamma, 0.1)
+    assert e.value.status == hmg.EINVAL
+    with pytest.raises(hmg.HmgError) as e:
+        hmg.Hierarchy(hmg.Options(dim=3, cells=(8, 8, 8), h=1 / 8, levels=2, smoother="rb"), np.ones(729), 10.0,
+                      np.zeros(729), 0.1)
+    assert e.value.status == hmg.EINVAL
+    # FD2 Jacobi with w^2 k^2 == 4/h^2 and no attenuation/shift: zero patch diagonal
+    h = 1 / 8
+    with pytest.raises(hmg.HmgError) as e:
+        hmg.Hierarchy(hmg.Options(dim=2, cells=(8, 8), h=h, levels=2, smoother="jacobi", fine_stencil="fd2",
+                                  damping=[0.8]), np.ones(81), 16.0, np.zeros(81), 0.0)
+    assert e.value.status == hmg.ESINGULAR_PATCH and "level 0" in str(e.value)
