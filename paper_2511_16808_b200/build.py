@@ -54,9 +54,9 @@ def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
     nvcc = _nvcc()
-    objs = []
     os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
-    for src in sources():
+
+    def compile_one(src):
         obj = os.path.join(PKG, "build", os.path.basename(src) + ".o")
         cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -68,7 +68,11 @@ def build(force=False, verbose=False):
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, sources()))
     tmp = LIB + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            *objs, "-o", tmp, "-lcudart"]

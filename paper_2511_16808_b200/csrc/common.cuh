@@ -39,6 +39,33 @@ template <typename T> __host__ __device__ __forceinline__ cplx<T> crecip(cplx<T>
   T d = b.x * b.x + b.y * b.y;
   return mkc<T>(b.x / d, -b.y / d);
 }
+// reciprocal / division with a correctly rounded fp32 reciprocal (MUFU + fixup)
+// instead of IEEE division; fp64 keeps the exact division.
+__device__ __forceinline__ float frcp(float d) { return __frcp_rn(d); }
+__device__ __forceinline__ double frcp(double d) { return 1.0 / d; }
+template <typename T> __device__ __forceinline__ cplx<T> crecip_fast(cplx<T> b) {
+  const T i = frcp(b.x * b.x + b.y * b.y);
+  return mkc<T>(b.x * i, -b.y * i);
+}
+template <typename T> __device__ __forceinline__ cplx<T> cdiv_fast(cplx<T> a, cplx<T> b) {
+  const T i = frcp(b.x * b.x + b.y * b.y);
+  return mkc<T>((a.x * b.x + a.y * b.y) * i, (a.y * b.x - a.x * b.y) * i);
+}
+// opaque select (selp): keeps pivot row swaps as register selects instead of
+// letting the optimiser rewrite them into dynamically indexed local memory
+__device__ __forceinline__ float selp(bool c, float a, float b) {
+  float r;
+  asm("{ .reg .pred q; setp.ne.b32 q, %3, 0; selp.f32 %0, %1, %2, q; }" : "=f"(r) : "f"(a), "f"(b), "r"((int)c));
+  return r;
+}
+__device__ __forceinline__ double selp(bool c, double a, double b) {
+  double r;
+  asm("{ .reg .pred q; setp.ne.b32 q, %3, 0; selp.f64 %0, %1, %2, q; }" : "=d"(r) : "d"(a), "d"(b), "r"((int)c));
+  return r;
+}
+template <typename T> __device__ __forceinline__ cplx<T> cselp(bool c, cplx<T> a, cplx<T> b) {
+  return mkc<T>(selp(c, a.x, b.x), selp(c, a.y, b.y));
+}
 template <typename T> __host__ __device__ __forceinline__ T cabs2(cplx<T> a) { return a.x * a.x + a.y * a.y; }
 
 template <typename To, typename From> __host__ __device__ __forceinline__ cplx<To> ccast(cplx<From> a) {

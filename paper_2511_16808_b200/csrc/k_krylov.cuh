@@ -1,15 +1,19 @@
-// k_krylov.cuh -- FGMRES BLAS-1: fused multi-dot,
-// multi-AXPY (+norm), scale and solution update, all over the contiguous
-// interior slab of the padded vectors (ghost entries are zero and stay zero).
+// k_krylov.cuh -- FGMRES BLAS-1: fused multi-dot
+// (+ self norm), multi-AXPY (+ norm), scale, all over the contiguous interior
+// slab of the padded vectors (ghost entries are zero and stay zero).
 // Dot products accumulate in fp64 for both precisions; reductions are
 // deterministic (fixed grid, per-block partials, fixed-order final pass).
+// The number of basis vectors NV is a compile-time parameter (dispatch in
+// hmg.cu), so each thread issues all NV loads of an element back to back:
+// the kernels are pure streams at HBM speed.
 #pragma once
 #include "common.cuh"
 
 namespace hmg {
 
 constexpr int KRY_THREADS = 256;
-constexpr int KRY_MAXV = 32;  // vectors per multi-dot / multi-axpy pass
+constexpr int KRY_MAXV = 32;      // partial-buffer rows: NV dots + 1 self norm
+constexpr int KRY_MAXBLK = 2048;  // partial-buffer columns (>= one full wave of blocks)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -17,46 +21,63 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// partial[i * nblk + block] = sum_e conj(V_i[e]) w[e],  i < nv
-template <typename TV, typename TW = TV>
-__global__ void __launch_bounds__(KRY_THREADS) k_multidot(const cplx<TV> *__restrict__ V, int64_t vstride, int nv,
+// partial[i * nblk + block] = sum_e conj(V_i[e]) w[e]   (i < NV)
+// partial[NV * nblk + block] = sum_e |w[e]|^2           (if SELF)
+template <typename TV, typename TW, int NV, bool SELF>
+__global__ void __launch_bounds__(KRY_THREADS) k_multidot(const cplx<TV> *__restrict__ V, int64_t vstride,
                                                           const cplx<TW> *__restrict__ w, int64_t len,
                                                           double2 *__restrict__ partial) {
-  double ar[KRY_MAXV], ai[KRY_MAXV];
+  constexpr int NA = NV + (SELF ? 1 : 0);
+  constexpr int U = NV <= 2 ? 4 : NV <= 5 ? 2 : 1;   // elements per thread per pass: >= ~8 loads in flight
+  double ar[NA], ai[NA];
 #pragma unroll
-  for (int i = 0; i < KRY_MAXV; ++i) ar[i] = ai[i] = 0.0;
+  for (int i = 0; i < NA; ++i) ar[i] = ai[i] = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += stride) {
-    const cplx<TW> wv = w[e];
-    const double wx = wv.x, wy = wv.y;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < len; e0 += stride * U) {
+    cplx<TV> v[U][NV];
+    cplx<TW> wv[U];
 #pragma unroll
-    for (int i = 0; i < KRY_MAXV; ++i) {
-      if (i < nv) {
-        const cplx<TV> v = V[(int64_t)i * vstride + e];
-        ar[i] = fma((double)v.x, wx, fma((double)v.y, wy, ar[i]));
-        ai[i] = fma((double)v.x, wy, fma(-(double)v.y, wx, ai[i]));
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < len) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[u][i] = V[(int64_t)i * vstride + e];
+        wv[u] = w[e];
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[u][i] = mkc<TV>(0, 0);
+        wv[u] = mkc<TW>(0, 0);
       }
     }
-  }
-  __shared__ double sr[KRY_THREADS / 32][KRY_MAXV], si[KRY_THREADS / 32][KRY_MAXV];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int i = 0; i < KRY_MAXV; ++i) {
-    if (i < nv) {
-      const double a = warp_sum(ar[i]), b = warp_sum(ai[i]);
-      if (lane == 0) { sr[wid][i] = a; si[wid][i] = b; }
+    for (int u = 0; u < U; ++u) {
+      const double wx = wv[u].x, wy = wv[u].y;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        ar[i] = fma((double)v[u][i].x, wx, fma((double)v[u][i].y, wy, ar[i]));
+        ai[i] = fma((double)v[u][i].x, wy, fma(-(double)v[u][i].y, wx, ai[i]));
+      }
+      if (SELF) ar[NV] = fma(wx, wx, fma(wy, wy, ar[NV]));
     }
   }
+  __shared__ double sr[KRY_THREADS / 32][NA], si[KRY_THREADS / 32][NA];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NA; ++i) {
+    const double a = warp_sum(ar[i]), b = warp_sum(ai[i]);
+    if (lane == 0) { sr[wid][i] = a; si[wid][i] = b; }
+  }
   __syncthreads();
-  if (threadIdx.x < nv) {
+  if (threadIdx.x < NA) {
     double a = 0, b = 0;
+#pragma unroll
     for (int k = 0; k < KRY_THREADS / 32; ++k) { a += sr[k][threadIdx.x]; b += si[k][threadIdx.x]; }
     partial[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = make_double2(a, b);
   }
 }
 
 // out[i] = sum_b partial[i * nblk + b]  (one warp per i, fixed order)
-__global__ void k_reduce_partials(const double2 *__restrict__ partial, int nblk, int nv, double2 *__restrict__ out) {
+static __global__ void k_reduce_partials(const double2 *__restrict__ partial, int nblk, int nv, double2 *__restrict__ out) {
   const int i = blockIdx.x;
   if (i >= nv) return;
   double a = 0, b = 0;
@@ -69,41 +90,55 @@ __global__ void k_reduce_partials(const double2 *__restrict__ partial, int nblk,
   if (threadIdx.x == 0) out[i] = make_double2(a, b);
 }
 
-// w <- w + sgn * sum_i coef[i] V_i  (coef on the device, fp64); if partial != nullptr
-// also partial[block] = sum |w_new|^2 (fp64)
-template <typename TV, typename TW = TV>
-__global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy(const cplx<TV> *__restrict__ V, int64_t vstride, int nv,
+// w <- w + sgn * sum_i coef[i] V_i  (coef on the device, fp64); if NORM also
+// partial[block] = sum |w_new|^2 (fp64, of the stored value)
+template <typename TV, typename TW, int NV, bool NORM>
+__global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy(const cplx<TV> *__restrict__ V, int64_t vstride,
                                                             const double2 *__restrict__ coef, double sgn,
                                                             cplx<TW> *__restrict__ w, int64_t len,
                                                             double2 *__restrict__ partial) {
-  __shared__ double2 sc[KRY_MAXV];
-  if (threadIdx.x < nv) sc[threadIdx.x] = make_double2(sgn * coef[threadIdx.x].x, sgn * coef[threadIdx.x].y);
+  __shared__ double2 sc[NV];
+  if (threadIdx.x < NV) sc[threadIdx.x] = make_double2(sgn * coef[threadIdx.x].x, sgn * coef[threadIdx.x].y);
   __syncthreads();
   double nrm = 0.0;
+  constexpr int U = NV <= 2 ? 4 : NV <= 5 ? 2 : 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += stride) {
-    const cplx<TW> wv = w[e];
-    double x = wv.x, y = wv.y;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < len; e0 += stride * U) {
+    cplx<TV> v[U][NV];
+    cplx<TW> wv[U];
 #pragma unroll
-    for (int i = 0; i < KRY_MAXV; ++i) {
-      if (i < nv) {
-        const cplx<TV> v = V[(int64_t)i * vstride + e];
-        const double2 c = sc[i];
-        x = fma(c.x, (double)v.x, fma(-c.y, (double)v.y, x));
-        y = fma(c.x, (double)v.y, fma(c.y, (double)v.x, y));
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < len) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[u][i] = V[(int64_t)i * vstride + e];
+        wv[u] = w[e];
       }
     }
-    const cplx<TW> o = mkc<TW>((TW)x, (TW)y);
-    w[e] = o;
-    nrm = fma((double)o.x, (double)o.x, fma((double)o.y, (double)o.y, nrm));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e >= len) continue;
+      double x = wv[u].x, y = wv[u].y;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const double2 c = sc[i];
+        x = fma(c.x, (double)v[u][i].x, fma(-c.y, (double)v[u][i].y, x));
+        y = fma(c.x, (double)v[u][i].y, fma(c.y, (double)v[u][i].x, y));
+      }
+      const cplx<TW> o = mkc<TW>((TW)x, (TW)y);
+      w[e] = o;
+      if (NORM) nrm = fma((double)o.x, (double)o.x, fma((double)o.y, (double)o.y, nrm));
+    }
   }
-  if (partial) {
+  if (NORM) {
     __shared__ double sn[KRY_THREADS / 32];
     nrm = warp_sum(nrm);
     if ((threadIdx.x & 31) == 0) sn[threadIdx.x >> 5] = nrm;
     __syncthreads();
     if (threadIdx.x == 0) {
       double a = 0;
+#pragma unroll
       for (int k = 0; k < KRY_THREADS / 32; ++k) a += sn[k];
       partial[blockIdx.x] = make_double2(a, 0.0);
     }
@@ -112,12 +147,17 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy(const cplx<TV> *__re
 
 // v <- s * w   (s real; optional precision conversion)
 template <typename TI, typename TO = TI>
-__global__ void k_scale(const cplx<TI> *__restrict__ w, cplx<TO> *__restrict__ v, double s, int64_t len) {
+__global__ void __launch_bounds__(KRY_THREADS) k_scale(const cplx<TI> *__restrict__ w, cplx<TO> *__restrict__ v,
+                                                       double s, int64_t len) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += stride) {
     const cplx<TI> a = w[e];
     v[e] = mkc<TO>((TO)(s * (double)a.x), (TO)(s * (double)a.y));
   }
 }
+
+#define HMG_NV_CASES(X) \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
+  X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31)
 
 }  // namespace hmg

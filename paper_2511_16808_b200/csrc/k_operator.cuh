@@ -40,48 +40,54 @@ template <> struct FineW<3, ST_FD2> {
 
 // y = A x   (f == nullptr)   or   y = f - A x   (residual), fine level.
 // sig[j] = sigma_j = (w^2k^2, -w^2k^2 g/w); alpha = shift (0 for H).
-template <typename T, int DIM, int KIND>
-__global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<T> *__restrict__ sig, T alpha, T ih2,
+// TC = arithmetic precision (T or double); storage of x, f, y stays T;
+// TS = storage precision of sigma.
+template <typename T, int DIM, int KIND, typename TC = T, typename TS = T>
+__global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<TS> *__restrict__ sig, TC alpha, TC ih2,
                                                  const cplx<T> *__restrict__ x,
                                                  const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y) {
   HMG_NODE_IDX(g, ix, iy, iz);
   using W = FineW<DIM, KIND>;
+  using CC = cplx<TC>;
   const int64_t i = g.idx(ix, iy, iz);
   const int64_t px = g.px;
-  const cplx<T> xc = x[i];
-  cplx<T> sf = cadd<T>(cadd<T>(x[i - 1], x[i + 1]), cadd<T>(x[i - px], x[i + px]));
-  cplx<T> se = mkc<T>(0, 0);
+  auto X = [&](int64_t k) { return ccast<TC, T>(x[k]); };
+  const CC xc = X(i);
+  CC sf = cadd<TC>(cadd<TC>(X(i - 1), X(i + 1)), cadd<TC>(X(i - px), X(i + px)));
+  CC se = mkc<TC>(0, 0);
   if (DIM == 2) {
-    if (W::Le != 0.0) se = cadd<T>(cadd<T>(x[i - px - 1], x[i - px + 1]), cadd<T>(x[i + px - 1], x[i + px + 1]));
+    if (W::Le != 0.0) se = cadd<TC>(cadd<TC>(X(i - px - 1), X(i - px + 1)), cadd<TC>(X(i + px - 1), X(i + px + 1)));
   } else {
     const int64_t pz = g.pxy;
-    sf = cadd<T>(sf, cadd<T>(x[i - pz], x[i + pz]));
+    sf = cadd<TC>(sf, cadd<TC>(X(i - pz), X(i + pz)));
     if (W::Le != 0.0) {
-      se = cadd<T>(cadd<T>(x[i - px - 1], x[i - px + 1]), cadd<T>(x[i + px - 1], x[i + px + 1]));
-      se = cadd<T>(se, cadd<T>(cadd<T>(x[i - pz - 1], x[i - pz + 1]), cadd<T>(x[i + pz - 1], x[i + pz + 1])));
-      se = cadd<T>(se, cadd<T>(cadd<T>(x[i - pz - px], x[i - pz + px]), cadd<T>(x[i + pz - px], x[i + pz + px])));
+      se = cadd<TC>(cadd<TC>(X(i - px - 1), X(i - px + 1)), cadd<TC>(X(i + px - 1), X(i + px + 1)));
+      se = cadd<TC>(se, cadd<TC>(cadd<TC>(X(i - pz - 1), X(i - pz + 1)), cadd<TC>(X(i + pz - 1), X(i + pz + 1))));
+      se = cadd<TC>(se, cadd<TC>(cadd<TC>(X(i - pz - px), X(i - pz + px)), cadd<TC>(X(i + pz - px), X(i + pz + px))));
     }
   }
   // L x
-  cplx<T> Lx = cscale<T>(xc, (T)W::Lc);
-  Lx = cfmar<T>(Lx, (T)W::Lf, sf);
-  if (W::Le != 0.0) Lx = cfmar<T>(Lx, (T)W::Le, se);
-  Lx = cscale<T>(Lx, ih2);
+  CC Lx = cscale<TC>(xc, (TC)W::Lc);
+  Lx = cfmar<TC>(Lx, (TC)W::Lf, sf);
+  if (W::Le != 0.0) Lx = cfmar<TC>(Lx, (TC)W::Le, se);
+  Lx = cscale<TC>(Lx, ih2);
   // M x
-  cplx<T> Mx = cscale<T>(xc, (T)W::Mc);
-  if (W::Mf != 0.0) Mx = cfmar<T>(Mx, (T)W::Mf, sf);
-  cplx<T> s = sig[i];
+  CC Mx = cscale<TC>(xc, (TC)W::Mc);
+  if (W::Mf != 0.0) Mx = cfmar<TC>(Mx, (TC)W::Mf, sf);
+  CC s = ccast<TC, TS>(sig[i]);
   s.y = fma(-alpha, s.x, s.y);
-  cplx<T> Ax = csub<T>(Lx, cmul<T>(s, Mx));
-  y[i] = f ? csub<T>(f[i], Ax) : Ax;
+  const CC Ax = csub<TC>(Lx, cmul<TC>(s, Mx));
+  y[i] = ccast<T, TC>(f ? csub<TC>(ccast<TC, T>(f[i]), Ax) : Ax);
 }
 
 // Stored stencil of radius R: coef[k][j], k = (ox+R) + (2R+1)((oy+R) + (2R+1)(oz+R)),
 // multiplies x[j + o].  Coefficients towards out-of-domain nodes are zero.
-template <typename T, int DIM, int R>
-__global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<T> *__restrict__ coef,
-                                                   const cplx<T> *__restrict__ x,
-                                                   const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y) {
+// TV = vector storage/arithmetic (fp64 on Galerkin levels), TK = coefficient storage.
+template <typename TV, typename TK, int DIM, int R>
+__global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__restrict__ coef,
+                                                   const cplx<TV> *__restrict__ x,
+                                                   const cplx<TV> *__restrict__ f, cplx<TV> *__restrict__ y) {
+  using T = TV;
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t i = g.idx(ix, iy, iz);
   constexpr int W = 2 * R + 1;
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<T> *__restr
     for (int oy = -R; oy <= R; ++oy)
 #pragma unroll
       for (int ox = -R; ox <= R; ++ox, ++k) {
-        const cplx<T> c = coef[(int64_t)k * g.total + i];
+        const cplx<T> c = ccast<T, TK>(coef[(int64_t)k * g.total + i]);
         acc = cfma<T>(acc, c, x[i + g.delta(ox, oy, oz)]);
       }
   (void)W;

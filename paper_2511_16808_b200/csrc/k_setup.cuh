@@ -139,7 +139,7 @@ __global__ void k_galerkin(Geo gf, Geo gc, const double2 *__restrict__ cf, int r
 
 // a7 (REDISCRETIZE): full-weighting average of a per-node field, normalised
 // by the in-domain weight sum (truncated lin R, reading A13).
-__global__ void k_fw_average(Geo gf, Geo gc, const double *__restrict__ ff, double *__restrict__ fc) {
+static __global__ void k_fw_average(Geo gf, Geo gc, const double *__restrict__ ff, double *__restrict__ fc) {
   HMG_NODE_IDX(gc, X, Y, Z);
   const double w1[3] = {0.25, 0.5, 0.25};
   const int zr = gc.dim == 3 ? 1 : 0;
@@ -253,7 +253,7 @@ __global__ void k_patch_inverse(Geo g, const double2 *__restrict__ coef, int r, 
 }
 
 // a8: dense coarsest matrix (row-major, compact x-fastest indices)
-__global__ void k_dense_assemble(Geo g, const double2 *__restrict__ coef, int r, double2 *__restrict__ A) {
+static __global__ void k_dense_assemble(Geo g, const double2 *__restrict__ coef, int r, double2 *__restrict__ A) {
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t N = g.nodes();
   const int64_t row = ((int64_t)iz * g.n[1] + iy) * g.n[0] + ix;
@@ -270,7 +270,7 @@ __global__ void k_dense_assemble(Geo g, const double2 *__restrict__ coef, int r,
 
 // Gauss-Jordan step k, part 1 (one block): partial pivot on column k, swap
 // rows, scale the pivot row, save the elimination factors fcol[i] = A[i][k].
-__global__ void k_gj_pivot(int N, int k, double2 *__restrict__ A, double2 *__restrict__ Ai,
+static __global__ void k_gj_pivot(int N, int k, double2 *__restrict__ A, double2 *__restrict__ Ai,
                            double2 *__restrict__ fcol, int *__restrict__ err) {
   __shared__ double sv[1024];
   __shared__ int si[1024];
@@ -311,7 +311,7 @@ __global__ void k_gj_pivot(int N, int k, double2 *__restrict__ A, double2 *__res
 }
 
 // Gauss-Jordan step k, part 2: eliminate column k from every other row.
-__global__ void k_gj_eliminate(int N, int k, double2 *__restrict__ A, double2 *__restrict__ Ai,
+static __global__ void k_gj_eliminate(int N, int k, double2 *__restrict__ A, double2 *__restrict__ Ai,
                                const double2 *__restrict__ fcol) {
   const int i = blockIdx.y;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;

@@ -21,10 +21,12 @@ template <> struct RW<2> {
   __device__ static constexpr double w(int k) { return k == 0 ? 0.375 : (k == 1 || k == -1) ? 0.25 : 0.0625; }
 };
 
-// fc[I] = sum_k w(k) r[2I + k]     (coarse-node parallel)
-template <typename T, int DIM, int RR>
-__global__ void __launch_bounds__(256) k_restrict(Geo gf, Geo gc, const cplx<T> *__restrict__ r,
-                                                  cplx<T> *__restrict__ fc) {
+// fc[I] = sum_k w(k) r[2I + k]     (coarse-node parallel; fp64 arithmetic,
+// TI/TO = storage of the fine input / coarse output)
+template <typename TI, typename TO, int DIM, int RR>
+__global__ void __launch_bounds__(256) k_restrict(Geo gf, Geo gc, const cplx<TI> *__restrict__ r,
+                                                  cplx<TO> *__restrict__ fc) {
+  using T = double;
   HMG_NODE_IDX(gc, X, Y, Z);
   const int64_t ic = gc.idx(X, Y, Z);
   const int64_t jf = gf.idx(2 * X, 2 * Y, DIM == 3 ? 2 * Z : 0);
@@ -37,12 +39,13 @@ __global__ void __launch_bounds__(256) k_restrict(Geo gf, Geo gc, const cplx<T> 
     for (int ky = -RR; ky <= RR; ++ky) {
       cplx<T> accx = mkc<T>(0, 0);
 #pragma unroll
-      for (int kx = -RR; kx <= RR; ++kx) accx = cfmar<T>(accx, (T)RW<RR>::w(kx), r[jf + gf.delta(kx, ky, kz)]);
+      for (int kx = -RR; kx <= RR; ++kx)
+        accx = cfmar<T>(accx, (T)RW<RR>::w(kx), ccast<T, TI>(r[jf + gf.delta(kx, ky, kz)]));
       accy = cfmar<T>(accy, (T)RW<RR>::w(ky), accx);
     }
     acc = DIM == 3 ? cfmar<T>(acc, (T)RW<RR>::w(kz), accy) : accy;
   }
-  fc[ic] = acc;
+  fc[ic] = ccast<TO, T>(acc);
 }
 
 // u[i] += sum_J P[i, J] e[J]     (fine-node parallel)
@@ -66,9 +69,10 @@ __device__ __forceinline__ int prolong_taps(int i, int *J, double *w) {
   return 2;
 }
 
-template <typename T, int DIM, int PR>
-__global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<T> *__restrict__ e,
-                                                     cplx<T> *__restrict__ u) {
+template <typename TE, typename TU, int DIM, int PR>
+__global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<TE> *__restrict__ e,
+                                                     cplx<TU> *__restrict__ u) {
+  using T = double;
   HMG_NODE_IDX(gf, ix, iy, iz);
   int Jx[3], Jy[3], Jz[3];
   double wx[3], wy[3], wz[3];
@@ -83,13 +87,13 @@ __global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<
     for (int b = 0; b < ny; ++b) {
       cplx<T> accx = mkc<T>(0, 0);
       const int64_t row = gc.base + (int64_t)Jz[c] * gc.pxy + (int64_t)Jy[b] * gc.px;
-      for (int a = 0; a < nx; ++a) accx = cfmar<T>(accx, (T)wx[a], e[row + Jx[a]]);
+      for (int a = 0; a < nx; ++a) accx = cfmar<T>(accx, (T)wx[a], ccast<T, TE>(e[row + Jx[a]]));
       accy = cfmar<T>(accy, (T)wy[b], accx);
     }
     acc = cfmar<T>(acc, (T)wz[c], accy);
   }
   const int64_t i = gf.idx(ix, iy, iz);
-  u[i] = cadd<T>(u[i], acc);
+  u[i] = ccast<TU, T>(cadd<T>(ccast<T, TU>(u[i]), acc));
 }
 
 }  // namespace hmg

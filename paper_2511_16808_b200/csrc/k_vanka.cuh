@@ -66,8 +66,8 @@ template <int DIM, int KIND> struct Patch {
 };
 
 // (1a) generic patch solve with stored inverses: y[a][c] = sum_b Hinv[a*K+b][c] r[c + o_b]
-template <typename T, int DIM, int KIND>
-__global__ void __launch_bounds__(256) k_patch_apply(Geo g, const cplx<T> *__restrict__ hinv,
+template <typename T, typename TK, int DIM, int KIND>
+__global__ void __launch_bounds__(256) k_patch_apply(Geo g, const cplx<TK> *__restrict__ hinv,
                                                      const cplx<T> *__restrict__ r, cplx<T> *__restrict__ y) {
   HMG_NODE_IDX(g, ix, iy, iz);
   using P = Patch<DIM, KIND>;
@@ -84,56 +84,311 @@ __global__ void __launch_bounds__(256) k_patch_apply(Geo g, const cplx<T> *__res
   for (int a = 0; a < P::K; ++a) {
     cplx<T> acc = mkc<T>(0, 0);
 #pragma unroll
-    for (int b = 0; b < P::K; ++b) acc = cfma<T>(acc, hinv[(int64_t)(a * P::K + b) * g.total + c], rv[b]);
+    for (int b = 0; b < P::K; ++b) acc = cfma<T>(acc, ccast<T, TK>(hinv[(int64_t)(a * P::K + b) * g.total + c]), rv[b]);
     y[(int64_t)a * g.total + c] = acc;
   }
 }
 
-// (1b) fine-level RB patch in closed form (2D).  With the compact stencil the
-// patch matrix is an arrow: leaf-leaf entries vanish (offsets (2,0),(2,2) lie
-// outside the 9-point support), centre-leaf = L's corner weight -1/(6h^2) (M
-// has no corner), diagonal a_j = Lc/h^2 - Mc sigma_s,j.  Hence
-//   y_c = (r_c - e sum_l r_l/a_l) / (a_c - e^2 sum_l 1/a_l),  y_l = (r_l - e y_c)/a_l.
-template <typename T, int KIND>
-__global__ void __launch_bounds__(256) k_patch_rb2d_fine(Geo g, const cplx<T> *__restrict__ sig, T alpha, T ih2,
-                                                         const cplx<T> *__restrict__ r, cplx<T> *__restrict__ y) {
-  HMG_NODE_IDX(g, ix, iy, iz);
+// (1b) fine-level RB smoothing sweep in ONE kernel (2D, matrix-free).
+// With the compact stencil the RB patch matrix is an arrow: leaf-leaf entries
+// vanish (offsets (2,0), (2,2) lie outside the 9-point support), centre-leaf =
+// L's corner weight e = -1/(6h^2) (M has no corner), diagonal a_j = Lc/h^2 -
+// Mc sigma_s,j.  Hence the patch solve of anchor c is
+//   y_c = (r_c - e sum_l r_l/a_l) / (a_c - e^2 sum_l 1/a_l),  y_l = (r_l - e y_c)/a_l,
+// and node j gathers  y_j + sum_{present diagonal anchors c} (r_j - e y_c)/a_j,
+// so only the CENTRE solutions need staging.  Per block: u on the tile + 3,
+// r and 1/a on the tile + 2, y_c on the tile + 1, all in shared memory; HBM
+// sees u, f, sigma read once and u written once (4 s per node; 3 s with
+// ZERO = zero initial guess, where r = f).
+template <typename TS, int KIND, int TX, int TY, bool ZERO>
+__global__ void __launch_bounds__(256) k_smooth_rb2d_fine(Geo g, const cplx<TS> *__restrict__ sig, double alpha_d,
+                                                          double ih2_d, const cplx<TS> *__restrict__ f,
+                                                          cplx<TS> *__restrict__ u, double w_d) {
+  // TS = storage of u, f, sigma and the precision of the (well-conditioned)
+  // closed-form patch algebra; the residual f - H_s u, where the compact
+  // stencil cancels ~1e2-1e3x, is always formed in fp64
+  using T = TS;
+  const T alpha = (T)alpha_d, ih2 = (T)ih2_d, w = (T)w_d;
   using W = FineW<2, KIND>;
-  const int64_t c = g.idx(ix, iy, iz);
+  constexpr int NT = 256;
+  constexpr int UX = TX + 6, UY = TY + 6, RX = TX + 4, RY = TY + 4, YX = TX + 2, YY = TY + 2;
+  constexpr int NU = (UX * UY + NT - 1) / NT, NR = (RX * RY + NT - 1) / NT;
+  __shared__ cplx<T> su[ZERO ? 1 : UY * UX];
+  __shared__ cplx<T> sr[RY * RX];   // f, then r
+  __shared__ cplx<T> sia[RY * RX];  // sigma, then 1/a
+  __shared__ cplx<T> syc[YY * YX];
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const T e = (T)W::Le * ih2;
-  auto diag = [&](int64_t j) {
-    cplx<T> s = sig[j];
-    s.y = fma(-alpha, s.x, s.y);
-    return mkc<T>((T)W::Lc * ih2 - (T)W::Mc * s.x, -(T)W::Mc * s.y);
-  };
-  const cplx<T> rc = r[c];
-  const cplx<T> ac = diag(c);
-  cplx<T> inva[4], rl[4];
-  bool present[4];
-  cplx<T> sr = mkc<T>(0, 0), si = mkc<T>(0, 0);
+  const cplx<T> zero = mkc<T>(0, 0);
+  // phase 1: every global load of the block, issued back to back
+  if (!ZERO) {
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int ox = (s & 1) ? 1 : -1, oy = (s & 2) ? 1 : -1;
-    present[s] = g.inside(ix + ox, iy + oy, 0);
-    inva[s] = mkc<T>(0, 0);
-    rl[s] = mkc<T>(0, 0);
-    if (present[s]) {
-      const int64_t j = c + g.delta(ox, oy, 0);
-      inva[s] = crecip<T>(diag(j));
-      rl[s] = r[j];
-      sr = cadd<T>(sr, cmul<T>(rl[s], inva[s]));
-      si = cadd<T>(si, inva[s]);
+    for (int k = 0; k < NU; ++k) {
+      const int i = tid + k * NT;
+      if (i < UY * UX) {
+        const int gx = x0 - 3 + i % UX, gy = y0 - 3 + i / UX;
+        su[i] = g.inside(gx, gy, 0) ? u[g.idx(gx, gy, 0)] : zero;
+      }
     }
   }
-  const cplx<T> num = mkc<T>(rc.x - e * sr.x, rc.y - e * sr.y);
-  const cplx<T> den = mkc<T>(ac.x - e * e * si.x, ac.y - e * e * si.y);
-  const cplx<T> yc = cdiv<T>(num, den);
-  y[c] = yc;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    cplx<T> v = mkc<T>(0, 0);
-    if (present[s]) v = cmul<T>(mkc<T>(rl[s].x - e * yc.x, rl[s].y - e * yc.y), inva[s]);
-    y[(int64_t)(s + 1) * g.total + c] = v;
+  for (int k = 0; k < NR; ++k) {
+    const int i = tid + k * NT;
+    if (i < RY * RX) {
+      const int gx = x0 - 2 + i % RX, gy = y0 - 2 + i / RX;
+      const bool in = g.inside(gx, gy, 0);
+      const int64_t j = g.idx(gx, gy, 0);
+      sr[i] = in ? f[j] : zero;
+      sia[i] = in ? sig[j] : zero;
+    }
+  }
+  __syncthreads();
+  // phase 2: r = f - H_s u and 1/a on the tile + 2 (in place)
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const int i = tid + k * NT;
+    if (i >= RY * RX) continue;
+    const int lx = i % RX, ly = i / RX;
+    if (!g.inside(x0 - 2 + lx, y0 - 2 + ly, 0)) { sia[i] = zero; continue; }
+    cplx<T> ss = sia[i];
+    ss.y = fma(-alpha, ss.x, ss.y);
+    const cplx<T> a = mkc<T>((T)W::Lc * ih2 - (T)W::Mc * ss.x, -(T)W::Mc * ss.y);
+    if (!ZERO) {
+      using Q = double;   // fp64 residual
+      auto U = [&](int k) { return ccast<Q, T>(su[(ly + 1) * UX + (lx + 1) + k]); };
+      const cplx<Q> uc = U(0);
+      const cplx<Q> sf = cadd<Q>(cadd<Q>(U(-1), U(1)), cadd<Q>(U(-UX), U(UX)));
+      cplx<Q> Lx = cscale<Q>(uc, (Q)W::Lc);
+      Lx = cfmar<Q>(Lx, (Q)W::Lf, sf);
+      if (W::Le != 0.0) {
+        const cplx<Q> se = cadd<Q>(cadd<Q>(U(-UX - 1), U(-UX + 1)), cadd<Q>(U(UX - 1), U(UX + 1)));
+        Lx = cfmar<Q>(Lx, (Q)W::Le, se);
+      }
+      Lx = cscale<Q>(Lx, ih2_d);
+      cplx<Q> Mx = cscale<Q>(uc, (Q)W::Mc);
+      if (W::Mf != 0.0) Mx = cfmar<Q>(Mx, (Q)W::Mf, sf);
+      cplx<Q> sq = ccast<Q, T>(sia[i]);
+      sq.y = fma(-alpha_d, sq.x, sq.y);
+      sr[i] = ccast<T, Q>(csub<Q>(ccast<Q, T>(sr[i]), csub<Q>(Lx, cmul<Q>(sq, Mx))));
+    }
+    sia[i] = crecip_fast<T>(a);
+  }
+  __syncthreads();
+  // phase 3: centre solutions of the patches anchored on the tile + 1
+  for (int i = tid; i < YY * YX; i += NT) {
+    const int lx = i % YX, ly = i / YX;
+    if (!g.inside(x0 - 1 + lx, y0 - 1 + ly, 0)) { syc[i] = zero; continue; }
+    const int ri = (ly + 1) * RX + (lx + 1);
+    // clipped leaves sit outside the domain, where sr = sia = 0: they drop out
+    const cplx<T> s_r = cadd<T>(cadd<T>(cmul<T>(sr[ri - RX - 1], sia[ri - RX - 1]), cmul<T>(sr[ri - RX + 1], sia[ri - RX + 1])),
+                                cadd<T>(cmul<T>(sr[ri + RX - 1], sia[ri + RX - 1]), cmul<T>(sr[ri + RX + 1], sia[ri + RX + 1])));
+    const cplx<T> s_i = cadd<T>(cadd<T>(sia[ri - RX - 1], sia[ri - RX + 1]), cadd<T>(sia[ri + RX - 1], sia[ri + RX + 1]));
+    const cplx<T> ac = crecip_fast<T>(sia[ri]);
+    const cplx<T> num = mkc<T>(sr[ri].x - e * s_r.x, sr[ri].y - e * s_r.y);
+    const cplx<T> den = mkc<T>(ac.x - e * e * s_i.x, ac.y - e * e * s_i.y);
+    syc[i] = cdiv_fast<T>(num, den);
+  }
+  __syncthreads();
+  // phase 4: gather and write
+  for (int oy = threadIdx.y; oy < TY; oy += blockDim.y) {
+    for (int ox = threadIdx.x; ox < TX; ox += blockDim.x) {
+      const int gx = x0 + ox, gy = y0 + oy;
+      if (!g.inside(gx, gy, 0)) continue;
+      const int yi = (oy + 1) * YX + (ox + 1);
+      cplx<T> syl = zero;
+      int k = 0;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int dx = (s & 1) ? 1 : -1, dy = (s & 2) ? 1 : -1;
+        if (g.inside(gx - dx, gy - dy, 0)) {
+          syl = cadd<T>(syl, syc[yi - dy * YX - dx]);
+          ++k;
+        }
+      }
+      const int ri = (oy + 2) * RX + (ox + 2);
+      const cplx<T> rj = sr[ri];
+      const cplx<T> lv = cmul<T>(mkc<T>((T)k * rj.x - e * syl.x, (T)k * rj.y - e * syl.y), sia[ri]);
+      const cplx<T> acc = cadd<T>(syc[yi], lv);
+      const cplx<T> upd = cscale<T>(acc, w / (T)(1 + k));
+      const int64_t j = g.idx(gx, gy, 0);
+      u[j] = ZERO ? upd : cadd<T>(su[(oy + 3) * UX + (ox + 3)], upd);
+    }
+  }
+}
+
+// Dense K x K complex solve A y = b in registers, Gaussian elimination with
+// partial pivoting (row swaps by static-index selects, so A stays in
+// registers); same pivoting rule as LAPACK getrf.  b is overwritten by y.
+template <typename T, int K>
+__device__ __forceinline__ void small_solve(cplx<T> (&A)[K][K], cplx<T> (&b)[K]) {
+  cplx<T> ipiv[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    T best = cabs2<T>(A[k][k]);
+    int p = k;
+#pragma unroll
+    for (int i = k + 1; i < K; ++i) {
+      const T v = cabs2<T>(A[i][k]);
+      if (v > best) { best = v; p = i; }
+    }
+#pragma unroll
+    for (int i = k + 1; i < K; ++i) {
+      const bool sw = i == p;   // branch-free select keeps A in registers
+#pragma unroll
+      for (int c = k; c < K; ++c) {
+        const cplx<T> t = A[k][c];
+        A[k][c] = cselp<T>(sw, A[i][c], t);
+        A[i][c] = cselp<T>(sw, t, A[i][c]);
+      }
+      const cplx<T> t = b[k];
+      b[k] = cselp<T>(sw, b[i], t);
+      b[i] = cselp<T>(sw, t, b[i]);
+    }
+    ipiv[k] = crecip_fast<T>(A[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < K; ++i) {
+      const cplx<T> f = cmul<T>(A[i][k], ipiv[k]);
+#pragma unroll
+      for (int c = k + 1; c < K; ++c) A[i][c] = csub<T>(A[i][c], cmul<T>(f, A[k][c]));
+      b[i] = csub<T>(b[i], cmul<T>(f, b[k]));
+    }
+  }
+#pragma unroll
+  for (int k = K - 1; k >= 0; --k) {
+    cplx<T> acc = b[k];
+#pragma unroll
+    for (int c = k + 1; c < K; ++c) acc = csub<T>(acc, cmul<T>(A[k][c], b[c]));
+    b[k] = cmul<T>(acc, ipiv[k]);
+  }
+}
+
+// (1c) one additive-Vanka sweep on a Galerkin level in ONE kernel (2D,
+// stored stencil of radius R): residual on the tile + 2 into shared memory,
+// every patch anchored on the tile + 1 assembled from the stencil
+// coefficients of its member rows (H_i = A[X_i, X_i], reading A8) and solved
+// in registers (no stored inverses), the K local values staged in shared
+// memory, then the 1/cnt-weighted gather.  HBM: the K stencil planes, u, f
+// read once, u written once (ZERO: f and the patch planes only).
+template <typename T, typename TK, int R, int KIND, int TX, int TY, bool ZERO, bool HINV>
+__global__ void __launch_bounds__(256, 2) k_smooth_stored2d(Geo g, const cplx<TK> *__restrict__ coef,
+                                                         const cplx<TK> *__restrict__ hinv,
+                                                         const cplx<T> *__restrict__ f, cplx<T> *__restrict__ u,
+                                                         T w) {
+  using P = Patch<2, KIND>;
+  constexpr int K = P::K;
+  constexpr int NT = 256;
+  constexpr int WS = 2 * R + 1;
+  constexpr int HU = 2 + R;
+  constexpr int UX = TX + 2 * HU, UY = TY + 2 * HU, RX = TX + 4, RY = TY + 4, YX = TX + 2, YY = TY + 2;
+  constexpr int NU = (UX * UY + NT - 1) / NT, NR = (RX * RY + NT - 1) / NT;
+  __shared__ cplx<T> su[ZERO ? 1 : UY * UX];
+  __shared__ cplx<T> sr[RY * RX];
+  __shared__ cplx<T> sy[K * YY * YX];
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const cplx<T> zero = mkc<T>(0, 0);
+  if (!ZERO) {
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      const int i = tid + k * NT;
+      if (i < UY * UX) {
+        const int gx = x0 - HU + i % UX, gy = y0 - HU + i / UX;
+        su[i] = g.inside(gx, gy, 0) ? u[g.idx(gx, gy, 0)] : zero;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const int i = tid + k * NT;
+    if (i < RY * RX) {
+      const int gx = x0 - 2 + i % RX, gy = y0 - 2 + i / RX;
+      sr[i] = g.inside(gx, gy, 0) ? f[g.idx(gx, gy, 0)] : zero;
+    }
+  }
+  __syncthreads();
+  if (!ZERO) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      const int i = tid + k * NT;
+      if (i >= RY * RX) continue;
+      const int lx = i % RX, ly = i / RX;
+      const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
+      if (!g.inside(gx, gy, 0)) continue;
+      const int64_t j = g.idx(gx, gy, 0);
+      const cplx<T> *uc = su + (ly + R) * UX + (lx + R);
+      cplx<T> acc = zero;
+#pragma unroll
+      for (int oy = -R; oy <= R; ++oy)
+#pragma unroll
+        for (int ox = -R; ox <= R; ++ox)
+          acc = cfma<T>(acc, ccast<T, TK>(coef[(int64_t)((ox + R) + WS * (oy + R)) * g.total + j]), uc[oy * UX + ox]);
+      sr[i] = csub<T>(sr[i], acc);
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < YY * YX; i += NT) {
+    const int lx = i % YX, ly = i / YX;
+    const int cx = x0 - 1 + lx, cy = y0 - 1 + ly;
+    if (!P::anchor(g, cx, cy, 0)) continue;
+    cplx<T> A[K][K], b[K];
+    bool pres[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      int ax, ay, az;
+      P::off(a, ax, ay, az);
+      pres[a] = g.inside(cx + ax, cy + ay, 0);
+      b[a] = pres[a] ? sr[(ly + 1 + ay) * RX + (lx + 1 + ax)] : zero;
+    }
+    if (HINV) {
+      // stored inverse of the clipped patch matrix (rows/cols of clipped members are 0)
+      const int64_t c = g.idx(cx, cy, 0);
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        cplx<T> acc = zero;
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc = cfma<T>(acc, ccast<T, TK>(hinv[(int64_t)(a * K + q) * g.total + c]), b[q]);
+        sy[a * YY * YX + i] = acc;
+      }
+      continue;
+    }
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      int ax, ay, az;
+      P::off(a, ax, ay, az);
+      const int64_t row = g.idx(cx + ax, cy + ay, 0);
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        int bx, by, bz;
+        P::off(c, bx, by, bz);
+        const int dx = bx - ax, dy = by - ay;
+        cplx<T> v = zero;
+        if (dx >= -R && dx <= R && dy >= -R && dy <= R && pres[a] && pres[c])
+          v = ccast<T, TK>(coef[(int64_t)((dx + R) + WS * (dy + R)) * g.total + row]);
+        if (!pres[a] && a == c) v = mkc<T>(1, 0);   // clipped member: identity row, zero rhs
+        A[a][c] = v;
+      }
+    }
+    small_solve<T, K>(A, b);
+#pragma unroll
+    for (int a = 0; a < K; ++a) sy[a * YY * YX + i] = b[a];
+  }
+  __syncthreads();
+  for (int oy = threadIdx.y; oy < TY; oy += blockDim.y) {
+    for (int ox = threadIdx.x; ox < TX; ox += blockDim.x) {
+      const int gx = x0 + ox, gy = y0 + oy;
+      if (!g.inside(gx, gy, 0)) continue;
+      cplx<T> acc = zero;
+#pragma unroll
+      for (int sI = 0; sI < K; ++sI) {
+        int dx, dy, dz;
+        P::off(sI, dx, dy, dz);
+        if (P::anchor(g, gx - dx, gy - dy, 0)) acc = cadd<T>(acc, sy[sI * YY * YX + (oy + 1 - dy) * YX + (ox + 1 - dx)]);
+      }
+      const cplx<T> upd = cscale<T>(acc, w / (T)P::count(g, gx, gy, 0));
+      const int64_t j = g.idx(gx, gy, 0);
+      u[j] = ZERO ? upd : cadd<T>(su[(oy + HU) * UX + (ox + HU)], upd);
+    }
   }
 }
 

@@ -1,0 +1,86 @@
+// krylov.cu -- compile-time-NV dispatch of the FGMRES BLAS-1 kernels
+// (k_krylov.cuh).  Separate translation unit: ~190 instantiations.
+#include "runtime.cuh"
+#include "k_krylov.cuh"
+
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
+namespace hmg {
+
+// Blocks of one full wave of `kernel` (occupancy API x SM count), capped by
+// the work and by the partial buffer: a grid-stride stream with no tail wave.
+template <typename K> static int wave_blocks(K kernel, int64_t len) {
+  static std::mutex mu;
+  static std::unordered_map<const void *, int> cache;
+  int per_sm;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find((const void *)kernel);
+    if (it == cache.end()) {
+      int nb = 0, dev = 0, sms = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, KRY_THREADS, 0));
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      it = cache.emplace((const void *)kernel, std::max(1, nb) * sms).first;
+    }
+    per_sm = it->second;
+  }
+  const int64_t need = (len + KRY_THREADS - 1) / KRY_THREADS;
+  return (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)per_sm, need, (int64_t)KRY_MAXBLK}));
+}
+
+template <typename TV, typename TW>
+int krylov_multidot(int nv, bool self, const cplx<TV> *V, int64_t vstride, const cplx<TW> *w, int64_t len,
+                    double2 *partial, cudaStream_t s) {
+  const dim3 b(KRY_THREADS);
+  if (self) {
+    switch (nv) {
+#define C_(N) case N: { auto k = k_multidot<TV, TW, N, true>; const int nb = wave_blocks(k, len); \
+                        launch(k, dim3(nb), b, 0, s, V, vstride, w, len, partial); return nb; }
+      HMG_NV_CASES(C_)
+#undef C_
+    }
+  } else {
+    switch (nv) {
+#define C_(N) case N: { auto k = k_multidot<TV, TW, N, false>; const int nb = wave_blocks(k, len); \
+                        launch(k, dim3(nb), b, 0, s, V, vstride, w, len, partial); return nb; }
+      HMG_NV_CASES(C_)
+#undef C_
+    }
+  }
+  throw HmgError(HMG_EINVAL, "multidot: vector count out of range");
+  return 0;
+}
+
+template <typename TV, typename TW>
+int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef, double sgn, cplx<TW> *w, int64_t len,
+                double2 *partial_norm, cudaStream_t s) {
+  const dim3 b(KRY_THREADS);
+  if (partial_norm) {
+    switch (nv) {
+#define C_(N) case N: { auto k = k_multi_axpy<TV, TW, N, true>; const int nb = wave_blocks(k, len); \
+                        launch(k, dim3(nb), b, 0, s, V, vstride, coef, sgn, w, len, partial_norm); return nb; }
+      HMG_NV_CASES(C_)
+#undef C_
+    }
+  } else {
+    switch (nv) {
+#define C_(N) case N: { auto k = k_multi_axpy<TV, TW, N, false>; const int nb = wave_blocks(k, len); \
+                        launch(k, dim3(nb), b, 0, s, V, vstride, coef, sgn, w, len, (double2 *)nullptr); return nb; }
+      HMG_NV_CASES(C_)
+#undef C_
+    }
+  }
+  throw HmgError(HMG_EINVAL, "multi_axpy: vector count out of range");
+  return 0;
+}
+
+template int krylov_multidot<float, float>(int, bool, const float2 *, int64_t, const float2 *, int64_t, double2 *, cudaStream_t);
+template int krylov_multidot<double, double>(int, bool, const double2 *, int64_t, const double2 *, int64_t, double2 *, cudaStream_t);
+template int krylov_axpy<float, float>(int, const float2 *, int64_t, const double2 *, double, float2 *, int64_t, double2 *, cudaStream_t);
+template int krylov_axpy<double, double>(int, const double2 *, int64_t, const double2 *, double, double2 *, int64_t, double2 *, cudaStream_t);
+template int krylov_axpy<float, double>(int, const float2 *, int64_t, const double2 *, double, double2 *, int64_t, double2 *, cudaStream_t);
+
+}  // namespace hmg

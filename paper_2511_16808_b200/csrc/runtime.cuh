@@ -1,0 +1,60 @@
+// runtime.cuh -- error type, launch helper and profiling hooks shared by the
+// host-side translation units of libhmg (hmg.cu, krylov.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "../../include/hmg.h"
+#include "common.cuh"
+
+namespace hmg {
+
+struct HmgError : std::runtime_error {
+  hmg_status st;
+  HmgError(hmg_status s, const std::string &m) : std::runtime_error(m), st(s) {}
+};
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      throw ::hmg::HmgError(e_ == cudaErrorMemoryAllocation ? HMG_ENOMEM : HMG_ECUDA,              \
+                            std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+  } while (0)
+
+// Tag the next launch with its kernel class, level and ALGORITHMIC bytes
+// (DESIGN.md §5); consumed by launch() when profiling is on.
+void tag(const char *name, int level, double bytes);
+int prof_before(cudaStream_t s);
+void prof_after(cudaStream_t s, int idx);
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args... args) {
+  if (g.x == 0 || g.y == 0 || g.z == 0) return;
+  const int pi = prof_before(s);
+  k<<<g, b, smem, s>>>(static_cast<KArgs>(args)...);
+  count_launch();
+  CK(cudaGetLastError());
+  prof_after(s, pi);
+}
+
+// Krylov launch dispatch (krylov.cu): nv is a runtime count in [1, 31]
+// mapped onto the compile-time NV of the kernels.
+// Each returns the number of blocks it launched (= partial columns written).
+template <typename TV, typename TW>
+int krylov_multidot(int nv, bool self, const cplx<TV> *V, int64_t vstride, const cplx<TW> *w, int64_t len,
+                    double2 *partial, cudaStream_t s);
+template <typename TV, typename TW>
+int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef, double sgn, cplx<TW> *w, int64_t len,
+                double2 *partial_norm, cudaStream_t s);
+
+// Fused Galerkin-level Vanka sweep, 2D (smooth2d.cu).
+// hinv == nullptr: patches factored on the fly in every sweep; else the
+// stored patch inverses are applied.
+template <typename T>
+void smooth_stored2d(int r, int kind, bool zero, const Geo &g, const cplx<T> *coef, const cplx<T> *hinv,
+                     const double2 *f, double2 *u, double w, cudaStream_t s);
+
+}  // namespace hmg
