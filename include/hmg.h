@@ -126,6 +126,45 @@ HMG_API hmg_status hmg_build_hierarchy(const hmg_options *opts, const double *ka
                                const double *gamma, double shift_alpha, void *stream,
                                hmg_hierarchy **out);
 
+/* ---- slab-partitioned solve over several GPUs ----------------
+ * The slowest axis (y in 2D, z in 3D) is cut into contiguous slabs, one per
+ * rank; coarse node I belongs to the rank owning fine node 2I; a level stays
+ * partitioned while every rank holds >= 2 G rows (G = ghost depth, 4), the
+ * rest (always including the coarsest) is replicated on every rank after an
+ * allgather.  Halos of the slab-axis ghost planes are exchanged before every
+ * neighbour-reading kernel; FGMRES dot products are allreduced (fp64 sum).
+ * Vectors passed to the calls below are the rank's own rows (hmg_level_rows)
+ * of the level, x-fastest, unpadded.  All calls on a distributed hierarchy
+ * are collective: every rank must make the same sequence of calls.
+ * Backends:
+ *   NCCL  -- one process per GPU: rank 0 gets an id (hmg_comm_nccl_unique_id),
+ *            broadcasts it out of band (e.g. torch.distributed), every rank
+ *            calls hmg_comm_nccl.  libnccl.so.2 is dlopen'ed (torch's copy if
+ *            already loaded).
+ *   LOCAL -- k virtual ranks on ONE GPU driven by k host threads (tests; bit-
+ *            parity of the partitioned algorithm with one slab): one group
+ *            (hmg_comm_local_group) and one handle per rank (hmg_comm_local_rank).
+ * Communicators are caller-owned and must outlive the hierarchies built on them. */
+typedef struct hmg_comm hmg_comm;
+HMG_API hmg_status hmg_comm_local_group(int nranks, hmg_comm **group);
+HMG_API hmg_status hmg_comm_local_rank(hmg_comm *group, int rank, hmg_comm **out);
+HMG_API hmg_status hmg_comm_nccl_unique_id(void *id128);            /* 128 bytes */
+HMG_API hmg_status hmg_comm_nccl(const void *id128, int rank, int nranks, hmg_comm **out);
+HMG_API void hmg_comm_destroy(hmg_comm *comm);
+/* As hmg_build_hierarchy, collectively on every rank of `comm`; kappa/gamma
+ * are the GLOBAL host arrays (setup is replicated, then sliced). */
+HMG_API hmg_status hmg_build_hierarchy_dist(const hmg_options *opts, const double *kappa, double omega,
+                                            const double *gamma, double shift_alpha, hmg_comm *comm,
+                                            void *stream, hmg_hierarchy **out);
+/* Global rows [lo, hi) of the slab axis this rank holds on `level` (0..N on
+ * replicated levels and on one GPU).  Returns 0, or -1 on bad arguments. */
+HMG_API int hmg_level_rows(const hmg_hierarchy *hier, int level, int64_t *lo, int64_t *hi);
+/* Host-only: the partition rule above for `nodes0` slab-axis nodes on level 0.
+ * lo/hi: [levels * nranks] (level-major), dist: [levels] (1 = partitioned).
+ * Returns the number of partitioned levels, or -1. */
+HMG_API int hmg_slab_partition(int64_t nodes0, int levels, int nranks, int ghost, int64_t *lo, int64_t *hi,
+                               int *dist);
+
 /* y = A_l x  (level 0: shifted ? H_s : H, matrix-free; level l>0: the stored
  * Galerkin stencil, shifted must be 1).  x, y: device vectors of level l's
  * node count (hmg_level_nodes).  Errors: HMG_EINVAL. */

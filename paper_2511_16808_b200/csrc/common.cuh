@@ -80,7 +80,9 @@ template <typename To, typename From> __host__ __device__ __forceinline__ cplx<T
 // reading A4/A5) costs no branch in the operator kernels.
 struct Geo {
   int dim;
-  int n[3];        // interior nodes per axis (n[2] = 1 in 2D)
+  int n[3];        // LOCAL interior nodes per axis (n[2] = 1 in 2D)
+  int N[3];        // GLOBAL nodes per axis (== n on one rank)
+  int o[3];        // global coordinate of local node 0 (nonzero only on the slab axis)
   int G;           // ghost width
   int64_t px;      // row pitch
   int64_t pxy;     // plane pitch
@@ -95,8 +97,12 @@ struct Geo {
   __host__ __device__ __forceinline__ int64_t delta(int ox, int oy, int oz) const {
     return (int64_t)oz * pxy + (int64_t)oy * px + ox;
   }
+  // is LOCAL node (x,y,z) inside the GLOBAL domain?  Every boundary decision
+  // (truncation, patch clipping, cnt_j) is taken in global coordinates, so a
+  // slab of a partitioned grid behaves exactly like the same rows of the whole.
   __host__ __device__ __forceinline__ bool inside(int x, int y, int z) const {
-    return x >= 0 && x < n[0] && y >= 0 && y < n[1] && z >= 0 && z < n[2];
+    x += o[0]; y += o[1]; z += o[2];
+    return x >= 0 && x < N[0] && y >= 0 && y < N[1] && z >= 0 && z < N[2];
   }
   __host__ __device__ __forceinline__ int64_t nodes() const { return (int64_t)n[0] * n[1] * n[2]; }
 };
@@ -107,6 +113,7 @@ inline Geo make_geo(int dim, const int64_t nodes[3], int G) {
   g.n[0] = (int)nodes[0];
   g.n[1] = (int)nodes[1];
   g.n[2] = dim == 3 ? (int)nodes[2] : 1;
+  for (int a = 0; a < 3; ++a) { g.N[a] = g.n[a]; g.o[a] = 0; }
   g.G = G;
   g.px = ((g.n[0] + 2 * G) + 7) / 8 * 8;
   g.pxy = g.px * (g.n[1] + 2 * G);

@@ -165,6 +165,7 @@ struct SolverBase {
   hmg_options opt{};
   std::vector<double> damping;
   int L = 0;
+  Comm *comm = nullptr;   // not owned; nullptr or size 1 = single GPU
   virtual void build(const double *kappa, double omega, const double *gamma, double alpha, cudaStream_t s) = 0;
   virtual void api_apply(int level, int shifted, const void *x, void *y, cudaStream_t s) = 0;
   virtual void api_residual(int level, int shifted, const void *f, const void *x, void *r, cudaStream_t s) = 0;
@@ -178,7 +179,38 @@ struct SolverBase {
   virtual int64_t level_nodes(int level, int64_t n[3]) const = 0;
   virtual int radius(int level) const = 0;
   virtual int copy_stencil(int level, double *out, int64_t cap) = 0;
+  virtual void level_rows(int level, int64_t *lo, int64_t *hi) const = 0;
 };
+
+// Slab partition: level-0 rows of the slowest axis split
+// evenly; coarse node I belongs to the rank owning fine node 2I, i.e.
+// [ceil(lo/2), ceil(hi/2)); a level is distributed while every rank holds at
+// least 2 G rows (so a halo of depth <= G comes from the adjacent rank only)
+// and all finer levels are distributed; the coarsest level is always
+// replicated.  lo/hi/dist are [levels * nranks] / [levels].
+static void slab_partition(const std::vector<int64_t> &Nl, int nranks, int G, std::vector<int64_t> &lo,
+                           std::vector<int64_t> &hi, std::vector<int> &dist) {
+  const int L = (int)Nl.size();
+  lo.assign((size_t)L * nranks, 0);
+  hi.assign((size_t)L * nranks, 0);
+  dist.assign(L, 0);
+  for (int r = 0; r < nranks; ++r) {
+    lo[r] = Nl[0] * r / nranks;
+    hi[r] = Nl[0] * (r + 1) / nranks;
+  }
+  for (int l = 1; l < L; ++l)
+    for (int r = 0; r < nranks; ++r) {
+      lo[(size_t)l * nranks + r] = (lo[(size_t)(l - 1) * nranks + r] + 1) / 2;
+      hi[(size_t)l * nranks + r] = (hi[(size_t)(l - 1) * nranks + r] + 1) / 2;
+    }
+  for (int l = 0; l < L - 1; ++l) {
+    if (nranks < 2 || (l > 0 && !dist[l - 1])) break;
+    bool ok = true;
+    for (int r = 0; r < nranks; ++r) ok = ok && hi[(size_t)l * nranks + r] - lo[(size_t)l * nranks + r] >= 2 * G;
+    if (!ok) break;
+    dist[l] = 1;
+  }
+}
 
 constexpr double kReorthEta2 = 0.01;  // ||w'||^2 < eta^2 ||w||^2 triggers a second CGS pass
 
@@ -193,6 +225,11 @@ template <typename T> struct Solver : SolverBase {
     DBuf coef;      // C [K][total] (levels > 0)
     DBuf hinv;      // C [k*k][total] (generic patch solve)
     DBuf u, f, r_, y;
+    bool dist = false;          // slab-partitioned (else replicated on every rank)
+    int64_t lo = 0, hi = 0;     // this rank's global rows on the slab axis
+    bool gather_in = false;     // first replicated level: filled by allgather
+    Geo view;                   // (gather_in) this rank's owned rows inside the replicated buffer
+    std::vector<size_t> goff, glen;   // (gather_in) per-rank byte ranges for the allgather (per element size 1)
   };
   std::vector<Level> lev;
   int G = 2;
@@ -201,6 +238,7 @@ template <typename T> struct Solver : SolverBase {
   DBuf sigd;              // fine-level sigma in fp64 (restart residual of FGMRES)
   DBuf ainv;              // coarsest inverse, double2 N_L x N_L
   bool rb_closed = false; // fine level uses the closed-form RB patch solve
+  DBuf rb_ia, rb_id;      // its sigma-only factors 1/a_j and 1/(a_c - e^2 sum 1/a_l), stored in T
   // FGMRES workspace
   int ws_m = 0;
   DBuf V, Z, partial, dres, io;
@@ -226,12 +264,15 @@ template <typename T> struct Solver : SolverBase {
     const int dim = opt.dim;
     L = opt.levels;
     G = opt.intergrid == HMG_CUBIC ? 3 : 2;
+    if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
     lev.resize(L);
     int64_t nodes[3] = {opt.cells[0] + 1, opt.cells[1] + 1, dim == 3 ? opt.cells[2] + 1 : 1};
     double h = opt.h;
     for (int l = 0; l < L; ++l) {
       lev[l].geo = make_geo(dim, nodes, G);
       lev[l].h = h;
+      lev[l].lo = 0;
+      lev[l].hi = nodes[dim == 3 ? 2 : 1];
       for (int a = 0; a < dim; ++a) nodes[a] = (nodes[a] - 1) / 2 + 1;
       h *= 2;
     }
@@ -310,9 +351,20 @@ template <typename T> struct Solver : SolverBase {
     for (int l = 0; l + 1 < L; ++l) {
       Level &Lv = lev[l];
       const int k = patch_size(dim, opt.smoother);
-      if (l == 0 && rb_closed) continue;   // fused closed-form sweep: no factors, no y planes
+      if (l == 0 && rb_closed) {   // fused closed-form sweep: two factor planes, no inverses, no y planes
+        rb_ia.alloc(Lv.geo.total * sizeof(C), s);
+        rb_id.alloc(Lv.geo.total * sizeof(C), s);
+        auto nl = node_launch(Lv.geo);
+        const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+        const double Lc = c4 ? FineW<2, ST_COMPACT4>::Lc : FineW<2, ST_FD2>::Lc;
+        const double Mc = c4 ? FineW<2, ST_COMPACT4>::Mc : FineW<2, ST_FD2>::Mc;
+        const double Le = c4 ? FineW<2, ST_COMPACT4>::Le : FineW<2, ST_FD2>::Le;
+        const double ih2 = 1.0 / (Lv.h * Lv.h);
+        launch(k_rb_factors<T>, nl.grid, nl.block, 0, s, Lv.geo, (const double2 *)sigd.template as<double2>(), alpha,
+               ih2, Lc, Mc, Le * ih2, rb_ia.template as<C>(), rb_id.template as<C>());
+        continue;
+      }
       Lv.hinv.alloc((size_t)k * k * Lv.geo.total * sizeof(C), s);
-      if (!fused_level(l)) Lv.y.alloc((size_t)k * Lv.geo.total * vsize(l), s);
       CK(cudaMemsetAsync(errb.p, 0xff, sizeof(unsigned long long), s));
       patch_inverse(Lv, cd[l], errb.template as<unsigned long long>(), s);
       unsigned long long bad = 0;
@@ -352,9 +404,12 @@ template <typename T> struct Solver : SolverBase {
       CK(cudaStreamSynchronize(s));
       if (bad) throw HmgError(HMG_ESINGULAR_COARSE, "coarsest Galerkin matrix is singular");
     }
+    if (comm && comm->size > 1) distribute(s);
     // cycle workspace
     for (int l = 0; l < L; ++l) {
       Level &Lv = lev[l];
+      const int k = patch_size(dim, opt.smoother);
+      if (!(l == 0 && rb_closed) && !fused_level(l) && l < L - 1) Lv.y.alloc((size_t)k * Lv.geo.total * vsize(l), s);
       Lv.u.alloc(Lv.geo.total * vsize(l), s);
       Lv.f.alloc(Lv.geo.total * vsize(l), s);
       Lv.r_.alloc(Lv.geo.total * vsize(l), s);
@@ -364,6 +419,93 @@ template <typename T> struct Solver : SolverBase {
     CK(cudaEventCreate(&ev1));
     CK(cudaMallocHost((void **)&hpin, 4096 * sizeof(double)));
     CK(cudaStreamSynchronize(s));
+  }
+
+  // ---------------------------------------------------------- distribution
+  int slab_axis() const { return opt.dim == 3 ? 2 : 1; }
+  int64_t rowsize(const Geo &g) const { return opt.dim == 3 ? g.pxy : g.px; }
+
+  // keep only this rank's slab (+ G ghost rows) of a per-node array of the
+  // replicated setup: rows [lo - G, hi + G) are contiguous in the padded box
+  void slice(DBuf &b, size_t esize, const Geo &gG, const Geo &gL, int64_t lo, cudaStream_t s) {
+    if (!b.p) return;
+    const size_t planes = b.bytes / (esize * gG.total);
+    DBuf nb;
+    nb.alloc(planes * gL.total * esize, s);
+    for (size_t k = 0; k < planes; ++k)
+      CK(cudaMemcpyAsync((char *)nb.p + k * gL.total * esize, (const char *)b.p + (k * gG.total + lo * rowsize(gG)) * esize,
+                         gL.total * esize, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    b = std::move(nb);
+  }
+
+  void distribute(cudaStream_t s) {
+    const int ax = slab_axis(), P = comm->size, me = comm->rank;
+    std::vector<int64_t> Nl(L), lo, hi;
+    std::vector<int> dist;
+    for (int l = 0; l < L; ++l) Nl[l] = lev[l].geo.N[ax];
+    slab_partition(Nl, P, G, lo, hi, dist);
+    for (int l = 0; l < L; ++l) {
+      Level &Lv = lev[l];
+      Lv.lo = 0;
+      Lv.hi = Nl[l];
+      if (!dist[l]) {
+        if (l > 0 && dist[l - 1]) {   // first replicated level: restricted rows are allgathered
+          Lv.gather_in = true;
+          Lv.view = Lv.geo;
+          const int64_t a = lo[(size_t)l * P + me], b = hi[(size_t)l * P + me];
+          Lv.view.n[ax] = (int)(b - a);
+          Lv.view.o[ax] = (int)a;
+          Lv.view.base += a * rowsize(Lv.geo);
+          Lv.goff.resize(P);
+          Lv.glen.resize(P);
+          for (int q = 0; q < P; ++q) {
+            Lv.goff[q] = (size_t)(G + lo[(size_t)l * P + q]) * rowsize(Lv.geo);
+            Lv.glen[q] = (size_t)(hi[(size_t)l * P + q] - lo[(size_t)l * P + q]) * rowsize(Lv.geo);
+          }
+        }
+        continue;
+      }
+      Lv.dist = true;
+      Lv.lo = lo[(size_t)l * P + me];
+      Lv.hi = hi[(size_t)l * P + me];
+      const Geo gG = Lv.geo;
+      Geo gL = gG;
+      gL.n[ax] = (int)(Lv.hi - Lv.lo);
+      gL.o[ax] = (int)Lv.lo;
+      gL.total = rowsize(gG) * (gL.n[ax] + 2 * G);
+      gL.slab_len = (int64_t)gL.n[ax] * rowsize(gG);
+      slice(Lv.coef, sizeof(C), gG, gL, Lv.lo, s);
+      slice(Lv.hinv, sizeof(C), gG, gL, Lv.lo, s);
+      if (l == 0) {
+        slice(sig, sizeof(C), gG, gL, Lv.lo, s);
+        slice(sigd, sizeof(D), gG, gL, Lv.lo, s);
+        slice(rb_ia, sizeof(C), gG, gL, Lv.lo, s);
+        slice(rb_id, sizeof(C), gG, gL, Lv.lo, s);
+        slice(w2k2, sizeof(double), gG, gL, Lv.lo, s);
+        slice(gq, sizeof(double), gG, gL, Lv.lo, s);
+      }
+      Lv.geo = gL;
+    }
+  }
+
+  // fill `depth` slab-axis ghost rows of `nplanes` planes of a level vector
+  // from the neighbouring ranks (no-op on replicated levels / one GPU)
+  void halo(int l, const void *vec, int depth, cudaStream_t s, int nplanes = 1, size_t esize = 0) {
+    const Level &Lv = lev[l];
+    if (!Lv.dist || !vec || depth <= 0) return;
+    if (!esize) esize = vsize(l);
+    const Geo &g = Lv.geo;
+    const int n = g.n[slab_axis()];
+    const size_t row = (size_t)rowsize(g) * esize;
+    for (int k = 0; k < nplanes; ++k) {
+      char *b = (char *)vec + (size_t)k * g.total * esize;
+      comm->halo(b + (size_t)G * row, b + (size_t)(G - depth) * row, b + (size_t)(G + n - depth) * row,
+                 b + (size_t)(G + n) * row, (size_t)depth * row, s);
+    }
+  }
+  void allreduce(double2 *d, int n, cudaStream_t s) {
+    if (comm && comm->size > 1) comm->allreduce_sum(reinterpret_cast<double *>(d), 2 * n, s);
   }
 
   // Galerkin levels of 2D hierarchies use the fused on-the-fly sweep
@@ -422,6 +564,7 @@ template <typename T> struct Solver : SolverBase {
   // y = A_l x  or  y = f - A_l x
   void op(int l, int shifted, const void *x, const void *f, void *y, cudaStream_t s) {
     const Level &Lv = lev[l];
+    halo(l, x, l == 0 ? 1 : Lv.r, s);
     auto nl = node_launch(Lv.geo);
     const double sz = vsize(l), nn = (double)Lv.geo.nodes();
     if (l == 0) {
@@ -458,15 +601,24 @@ template <typename T> struct Solver : SolverBase {
 
   template <typename TI> void restrict_t(int l, const TI *r, D *fc, cudaStream_t s) {
     const Level &F = lev[l], &Cc = lev[l + 1];
-    auto nl = node_launch(Cc.geo);
+    halo(l, r, F.rR, s);
+    // into the first replicated level: compute this rank's rows, then allgather
+    const Geo &gc = Cc.gather_in ? Cc.view : Cc.geo;
+    auto nl = node_launch(gc);
     using BI = decltype(r->x);
-    tag("restrict", l, (double)sizeof(TI) * F.geo.nodes() + (double)sizeof(D) * Cc.geo.nodes());
+    tag("restrict", l, (double)sizeof(TI) * F.geo.nodes() + (double)sizeof(D) * gc.nodes());
     if (opt.dim == 2) {
-      if (F.rR == 1) launch(k_restrict<BI, double, 2, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, r, fc);
-      else launch(k_restrict<BI, double, 2, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, r, fc);
+      if (F.rR == 1) launch(k_restrict<BI, double, 2, 1>, nl.grid, nl.block, 0, s, F.geo, gc, r, fc);
+      else launch(k_restrict<BI, double, 2, 2>, nl.grid, nl.block, 0, s, F.geo, gc, r, fc);
     } else {
-      if (F.rR == 1) launch(k_restrict<BI, double, 3, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, r, fc);
-      else launch(k_restrict<BI, double, 3, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, r, fc);
+      if (F.rR == 1) launch(k_restrict<BI, double, 3, 1>, nl.grid, nl.block, 0, s, F.geo, gc, r, fc);
+      else launch(k_restrict<BI, double, 3, 2>, nl.grid, nl.block, 0, s, F.geo, gc, r, fc);
+    }
+    if (Cc.gather_in) {
+      std::vector<size_t> off(Cc.goff), len(Cc.glen);
+      for (auto &x : off) x *= sizeof(D);
+      for (auto &x : len) x *= sizeof(D);
+      comm->allgatherv(fc, off, len, s);
     }
   }
   void restrict_(int l, const void *r, void *fc, cudaStream_t s) {
@@ -476,6 +628,7 @@ template <typename T> struct Solver : SolverBase {
 
   template <typename TU> void prolong_t(int l, const D *e, TU *u, cudaStream_t s) {
     const Level &F = lev[l], &Cc = lev[l + 1];
+    halo(l + 1, e, 1, s);
     auto nl = node_launch(F.geo);
     using BU = decltype(u->x);
     tag("prolong_add", l, 2.0 * sizeof(TU) * F.geo.nodes() + (double)sizeof(D) * Cc.geo.nodes());
@@ -500,9 +653,11 @@ template <typename T> struct Solver : SolverBase {
     TV *y = Lv.y.template as<TV>();
     constexpr int K = Patch<DIM, KIND>::K;
     const double nn = (double)Lv.geo.nodes();
+    halo(l, r, 1, s);
     tag("patch_apply", l, ((double)K * K * sizeof(C) + (K + 1) * sizeof(TV)) * nn);
     launch(k_patch_apply<BV, T, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)Lv.hinv.template as<C>(),
            (const TV *)r, y);
+    halo(l, y, 1, s, K);
     tag("vanka_gather", l, (K + (zero ? 1 : 2)) * sizeof(TV) * nn);
     launch(k_vanka_gather<BV, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const TV *)y, (BV)damp(l), (TV *)u, zero);
   }
@@ -522,28 +677,32 @@ template <typename T> struct Solver : SolverBase {
     const double w = damp(l);
     const double nn = (double)Lv.geo.nodes();
     if (l == 0 && rb_closed) {
-      // (residual formed in fp64 inside the kernel; closed-form patch algebra in T)
       // fused sweep: residual (unless zero), closed-form patch solves, gather; fp64 arithmetic
       const double ih2 = 1.0 / (Lv.h * Lv.h);
-      constexpr int TX = 32, TY = 16;
+      constexpr int TX = 32, TY = sizeof(T) == 8 ? 8 : 16;   // fp64 storage: 32 x 8 tiles keep smem < 48 KB
       dim3 grid((Lv.geo.n[0] + TX - 1) / TX, (Lv.geo.n[1] + TY - 1) / TY), block(32, 8);
       const C *sg = sig.template as<C>();
+      const C *ia = rb_ia.template as<C>(), *id = rb_id.template as<C>();
       const C *ff = (const C *)f;
       C *uu = (C *)u;
-      tag(zero ? "smooth_rb2d_fine_zero" : "smooth_rb2d_fine", 0, (zero ? 3 : 4) * sizeof(C) * nn);
+      if (!zero) halo(0, u, 3, s);
+      halo(0, f, 2, s);
+      tag(zero ? "smooth_rb2d_fine_zero" : "smooth_rb2d_fine", 0, (zero ? 4 : 6) * sizeof(C) * nn);
       const bool c4 = opt.fine_stencil == HMG_COMPACT4;
       if (zero) {
-        if (c4) launch(k_smooth_rb2d_fine<T, ST_COMPACT4, TX, TY, true>, grid, block, 0, s, Lv.geo, sg, alpha, ih2, ff, uu, w);
-        else launch(k_smooth_rb2d_fine<T, ST_FD2, TX, TY, true>, grid, block, 0, s, Lv.geo, sg, alpha, ih2, ff, uu, w);
+        if (c4) launch(k_smooth_rb2d_fine<T, ST_COMPACT4, TX, TY, true>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, uu, w);
+        else launch(k_smooth_rb2d_fine<T, ST_FD2, TX, TY, true>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, uu, w);
       } else {
-        if (c4) launch(k_smooth_rb2d_fine<T, ST_COMPACT4, TX, TY, false>, grid, block, 0, s, Lv.geo, sg, alpha, ih2, ff, uu, w);
-        else launch(k_smooth_rb2d_fine<T, ST_FD2, TX, TY, false>, grid, block, 0, s, Lv.geo, sg, alpha, ih2, ff, uu, w);
+        if (c4) launch(k_smooth_rb2d_fine<T, ST_COMPACT4, TX, TY, false>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, uu, w);
+        else launch(k_smooth_rb2d_fine<T, ST_FD2, TX, TY, false>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, uu, w);
       }
       return;
     }
     if (fused_level(l)) {
       const int K = patch_size(opt.dim, opt.smoother);
       const double planes = zero ? (K > 1 ? 13.0 : 1.0) : (double)kcount(opt.dim, Lv.r);
+      if (!zero) halo(l, u, 2 + Lv.r, s);
+      halo(l, f, 2, s);
       const double hplanes = Lv.hinv.p ? (double)K * K : 0.0;
       tag(zero ? "smooth_stored_zero" : "smooth_stored", l,
           ((Lv.hinv.p ? (zero ? 0.0 : kcount(opt.dim, Lv.r)) : planes) + hplanes) * sizeof(C) * nn +
@@ -693,6 +852,7 @@ template <typename T> struct Solver : SolverBase {
     tag("reduce", 0, 16.0 * (nv + self) * nb);
     launch(k_reduce_partials, dim3(nv + self), dim3(32), 0, s, (const double2 *)partial.template as<double2>(), nb,
            nv + (int)self, out);
+    allreduce(out, nv + (int)self, s);
   }
   template <typename TV, typename TW>
   void maxpy(const cplx<TV> *Vb, int nv, const double2 *coef, double sgn, cplx<TW> *w, double2 *nrm_out,
@@ -705,6 +865,7 @@ template <typename T> struct Solver : SolverBase {
       tag("reduce", 0, 16.0 * nb);
       launch(k_reduce_partials, dim3(1), dim3(32), 0, s, (const double2 *)partial.template as<double2>(), nb, 1,
              nrm_out);
+      allreduce(nrm_out, 1, s);
     }
   }
   template <typename TX> double norm(const cplx<TX> *x, cudaStream_t s) {
@@ -727,6 +888,7 @@ template <typename T> struct Solver : SolverBase {
   // smooth vectors: either would cap the attainable relres near the 1e-6 tol.)
   void matvec(const C *z, C *w, cudaStream_t s) {
     const Level &Lv = lev[0];
+    halo(0, z, 1, s);
     auto nl = node_launch(Lv.geo);
     const double ih2 = 1.0 / (Lv.h * Lv.h);
     const double2 *sg = sigd.template as<double2>();
@@ -744,6 +906,7 @@ template <typename T> struct Solver : SolverBase {
   // rd = qd - H xd in fp64 (unshifted fine operator)
   void residual_d(cudaStream_t s) {
     const Level &Lv = lev[0];
+    halo(0, xd.p, 1, s, 1, sizeof(D));
     auto nl = node_launch(Lv.geo);
     const double ih2 = 1.0 / (Lv.h * Lv.h);
     const double2 *sg = sigd.template as<double2>();
@@ -928,6 +1091,11 @@ template <typename T> struct Solver : SolverBase {
     return g.nodes();
   }
   int radius(int l) const override { return (l < 0 || l >= L) ? -1 : lev[l].r; }
+  void level_rows(int l, int64_t *lo, int64_t *hi) const override {
+    if (l < 0 || l >= L) { *lo = *hi = -1; return; }
+    *lo = lev[l].lo;
+    *hi = lev[l].hi;
+  }
   int copy_stencil(int l, double *out, int64_t cap) override {
     check_level(l);
     cudaStream_t s = 0;
@@ -956,6 +1124,11 @@ struct hmg_hierarchy {
   std::unique_ptr<hmg::SolverBase> impl;
 };
 
+struct hmg_comm {
+  std::shared_ptr<void> group;            // LOCAL group (shared by its rank handles)
+  std::unique_ptr<hmg::Comm> comm;        // a rank's communicator (null for a group handle)
+};
+
 static thread_local std::string t_err;
 
 static hmg_status fail(hmg_status s, const std::string &m) {
@@ -974,8 +1147,81 @@ static cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 extern "C" {
 
+static hmg_status build_impl(const hmg_options *o, const double *kappa, double omega, const double *gamma,
+                             double alpha, hmg::Comm *comm, void *stream, hmg_hierarchy **out);
+
 hmg_status hmg_build_hierarchy(const hmg_options *o, const double *kappa, double omega, const double *gamma,
                                double alpha, void *stream, hmg_hierarchy **out) {
+  return build_impl(o, kappa, omega, gamma, alpha, nullptr, stream, out);
+}
+
+hmg_status hmg_build_hierarchy_dist(const hmg_options *o, const double *kappa, double omega, const double *gamma,
+                                    double alpha, hmg_comm *comm, void *stream, hmg_hierarchy **out) {
+  if (!comm || !comm->comm) return fail(HMG_EINVAL, "comm must be a rank communicator");
+  return build_impl(o, kappa, omega, gamma, alpha, comm->comm.get(), stream, out);
+}
+
+hmg_status hmg_comm_local_group(int nranks, hmg_comm **out) {
+  HMG_API_BEGIN
+  if (!out || nranks < 1) return fail(HMG_EINVAL, "bad arguments");
+  std::unique_ptr<hmg_comm> c(new hmg_comm);
+  c->group = hmg::local_group_create(nranks);
+  *out = c.release();
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_comm_local_rank(hmg_comm *group, int rank, hmg_comm **out) {
+  HMG_API_BEGIN
+  if (!group || !group->group || !out) return fail(HMG_EINVAL, "bad arguments");
+  std::unique_ptr<hmg_comm> c(new hmg_comm);
+  c->comm.reset(hmg::local_comm_create(group->group, rank));
+  *out = c.release();
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_comm_nccl_unique_id(void *id128) {
+  HMG_API_BEGIN
+  if (!id128) return fail(HMG_EINVAL, "null pointer");
+  hmg::nccl_unique_id(id128);
+  return HMG_OK;
+  HMG_API_END
+}
+
+hmg_status hmg_comm_nccl(const void *id128, int rank, int nranks, hmg_comm **out) {
+  HMG_API_BEGIN
+  if (!id128 || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(HMG_EINVAL, "bad arguments");
+  std::unique_ptr<hmg_comm> c(new hmg_comm);
+  c->comm.reset(hmg::nccl_comm_create(id128, rank, nranks));
+  *out = c.release();
+  return HMG_OK;
+  HMG_API_END
+}
+
+void hmg_comm_destroy(hmg_comm *c) { delete c; }
+
+int hmg_slab_partition(int64_t nodes0, int levels, int nranks, int ghost, int64_t *lo, int64_t *hi, int *dist) {
+  if (nodes0 < 1 || levels < 1 || nranks < 1 || ghost < 1 || !lo || !hi || !dist) return -1;
+  std::vector<int64_t> Nl(levels), l2, h2;
+  std::vector<int> d2;
+  Nl[0] = nodes0;
+  for (int l = 1; l < levels; ++l) Nl[l] = (Nl[l - 1] - 1) / 2 + 1;
+  hmg::slab_partition(Nl, nranks, ghost, l2, h2, d2);
+  for (size_t i = 0; i < l2.size(); ++i) { lo[i] = l2[i]; hi[i] = h2[i]; }
+  int nd = 0;
+  for (int l = 0; l < levels; ++l) { dist[l] = d2[l]; nd += d2[l]; }
+  return nd;
+}
+
+int hmg_level_rows(const hmg_hierarchy *h, int level, int64_t *lo, int64_t *hi) {
+  if (!h || !lo || !hi || level < 0 || level >= h->impl->L) return -1;
+  h->impl->level_rows(level, lo, hi);
+  return 0;
+}
+
+static hmg_status build_impl(const hmg_options *o, const double *kappa, double omega, const double *gamma,
+                             double alpha, hmg::Comm *comm, void *stream, hmg_hierarchy **out) {
   HMG_API_BEGIN
   if (!o || !kappa || !gamma || !out) return fail(HMG_EINVAL, "null pointer");
   *out = nullptr;
@@ -1009,6 +1255,7 @@ hmg_status hmg_build_hierarchy(const hmg_options *o, const double *kappa, double
   h->impl->opt = *o;
   h->impl->damping.assign(o->damping, o->damping + o->n_damping);
   h->impl->opt.damping = nullptr;
+  h->impl->comm = comm;
   h->impl->build(kappa, omega, gamma, alpha, S(stream));
   *out = h.release();
   return HMG_OK;

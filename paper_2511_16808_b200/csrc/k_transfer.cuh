@@ -29,7 +29,9 @@ __global__ void __launch_bounds__(256) k_restrict(Geo gf, Geo gc, const cplx<TI>
   using T = double;
   HMG_NODE_IDX(gc, X, Y, Z);
   const int64_t ic = gc.idx(X, Y, Z);
-  const int64_t jf = gf.idx(2 * X, 2 * Y, DIM == 3 ? 2 * Z : 0);
+  // coarse node I (global) sits on fine node 2I (global); map to fine-local
+  const int64_t jf = gf.idx(2 * (X + gc.o[0]) - gf.o[0], 2 * (Y + gc.o[1]) - gf.o[1],
+                            DIM == 3 ? 2 * (Z + gc.o[2]) - gf.o[2] : 0);
   constexpr int ZR = DIM == 3 ? RR : 0;
   cplx<T> acc = mkc<T>(0, 0);
 #pragma unroll
@@ -76,11 +78,16 @@ __global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<
   HMG_NODE_IDX(gf, ix, iy, iz);
   int Jx[3], Jy[3], Jz[3];
   double wx[3], wy[3], wz[3];
-  const int nx = prolong_taps<PR>(ix, Jx, wx);
-  const int ny = prolong_taps<PR>(iy, Jy, wy);
+  // taps from GLOBAL fine coordinates (parity decides), then coarse-local indices
+  const int nx = prolong_taps<PR>(ix + gf.o[0], Jx, wx);
+  const int ny = prolong_taps<PR>(iy + gf.o[1], Jy, wy);
   int nz = 1;
   Jz[0] = 0; wz[0] = 1.0;
-  if (DIM == 3) nz = prolong_taps<PR>(iz, Jz, wz);
+  if (DIM == 3) nz = prolong_taps<PR>(iz + gf.o[2], Jz, wz);
+  for (int a = 0; a < nx; ++a) Jx[a] -= gc.o[0];
+  for (int b = 0; b < ny; ++b) Jy[b] -= gc.o[1];
+  if (DIM == 3)
+    for (int c = 0; c < nz; ++c) Jz[c] -= gc.o[2];
   cplx<T> acc = mkc<T>(0, 0);
   for (int c = 0; c < nz; ++c) {
     cplx<T> accy = mkc<T>(0, 0);

@@ -42,8 +42,9 @@ template <int DIM, int KIND> struct Patch {
   // is c a patch anchor?
   __host__ __device__ static __forceinline__ bool anchor(const Geo &g, int x, int y, int z) {
     if (KIND == PK_ELEMENT) {
-      bool ok = x >= 0 && x < g.n[0] - 1 && y >= 0 && y < g.n[1] - 1;
-      if (DIM == 3) ok = ok && z >= 0 && z < g.n[2] - 1;
+      x += g.o[0]; y += g.o[1]; z += g.o[2];
+      bool ok = x >= 0 && x < g.N[0] - 1 && y >= 0 && y < g.N[1] - 1;
+      if (DIM == 3) ok = ok && z >= 0 && z < g.N[2] - 1;
       return ok;
     }
     return g.inside(x, y, z);
@@ -51,8 +52,9 @@ template <int DIM, int KIND> struct Patch {
   // cnt_j = number of patches containing node j
   __host__ __device__ static __forceinline__ int count(const Geo &g, int x, int y, int z) {
     if (KIND == PK_ELEMENT) {
-      int c = ((x >= 1) + (x <= g.n[0] - 2)) * ((y >= 1) + (y <= g.n[1] - 2));
-      if (DIM == 3) c *= (z >= 1) + (z <= g.n[2] - 2);
+      x += g.o[0]; y += g.o[1]; z += g.o[2];
+      int c = ((x >= 1) + (x <= g.N[0] - 2)) * ((y >= 1) + (y <= g.N[1] - 2));
+      if (DIM == 3) c *= (z >= 1) + (z <= g.N[2] - 2);
       return c;
     }
     int c = 0;
@@ -96,31 +98,54 @@ __global__ void __launch_bounds__(256) k_patch_apply(Geo g, const cplx<TK> *__re
 // Mc sigma_s,j.  Hence the patch solve of anchor c is
 //   y_c = (r_c - e sum_l r_l/a_l) / (a_c - e^2 sum_l 1/a_l),  y_l = (r_l - e y_c)/a_l,
 // and node j gathers  y_j + sum_{present diagonal anchors c} (r_j - e y_c)/a_j,
-// so only the CENTRE solutions need staging.  Per block: u on the tile + 3,
-// r and 1/a on the tile + 2, y_c on the tile + 1, all in shared memory; HBM
-// sees u, f, sigma read once and u written once (4 s per node; 3 s with
-// ZERO = zero initial guess, where r = f).
+// so only the CENTRE solutions need staging.  The two sigma-only factors
+// ia_j = 1/a_j and id_c = 1/(a_c - e^2 sum_l ia_l) are precomputed at setup
+// (k_rb_factors, stored in TS like every other coefficient): the sweep has no
+// division and all its arithmetic is fp64.  Per block: u on the tile + 3,
+// r / ia on the tile + 2, y_c on the tile + 1, all in shared memory; HBM sees
+// u, f, sigma, ia, id read once and u written once (6 TS per node; 4 with
+// ZERO = zero initial guess, where r = f and sigma is not needed).
+template <typename TS>
+__global__ void k_rb_factors(Geo g, const double2 *__restrict__ sigd, double alpha, double ih2, double Lc, double Mc,
+                             double e, cplx<TS> *__restrict__ ia, cplx<TS> *__restrict__ id) {
+  HMG_NODE_IDX(g, ix, iy, iz);
+  auto diag = [&](int x, int y) {
+    double2 s = sigd[g.idx(x, y, 0)];
+    s.y = fma(-alpha, s.x, s.y);
+    return make_double2(Lc * ih2 - Mc * s.x, -Mc * s.y);
+  };
+  const double2 ac = diag(ix, iy);
+  double2 si = make_double2(0, 0);
+  for (int s = 0; s < 4; ++s) {
+    const int dx = (s & 1) ? 1 : -1, dy = (s & 2) ? 1 : -1;
+    if (g.inside(ix + dx, iy + dy, 0)) si = cadd<double>(si, crecip<double>(diag(ix + dx, iy + dy)));
+  }
+  const int64_t j = g.idx(ix, iy, 0);
+  ia[j] = ccast<TS, double>(crecip<double>(ac));
+  id[j] = ccast<TS, double>(crecip<double>(make_double2(ac.x - e * e * si.x, ac.y - e * e * si.y)));
+}
+
 template <typename TS, int KIND, int TX, int TY, bool ZERO>
-__global__ void __launch_bounds__(256) k_smooth_rb2d_fine(Geo g, const cplx<TS> *__restrict__ sig, double alpha_d,
-                                                          double ih2_d, const cplx<TS> *__restrict__ f,
-                                                          cplx<TS> *__restrict__ u, double w_d) {
-  // TS = storage of u, f, sigma and the precision of the (well-conditioned)
-  // closed-form patch algebra; the residual f - H_s u, where the compact
-  // stencil cancels ~1e2-1e3x, is always formed in fp64
-  using T = TS;
-  const T alpha = (T)alpha_d, ih2 = (T)ih2_d, w = (T)w_d;
+__global__ void __launch_bounds__(256) k_smooth_rb2d_fine(Geo g, const cplx<TS> *__restrict__ sig,
+                                                          const cplx<TS> *__restrict__ ia,
+                                                          const cplx<TS> *__restrict__ id, double alpha, double ih2,
+                                                          const cplx<TS> *__restrict__ f, cplx<TS> *__restrict__ u,
+                                                          double w) {
   using W = FineW<2, KIND>;
+  using T = double;
   constexpr int NT = 256;
   constexpr int UX = TX + 6, UY = TY + 6, RX = TX + 4, RY = TY + 4, YX = TX + 2, YY = TY + 2;
   constexpr int NU = (UX * UY + NT - 1) / NT, NR = (RX * RY + NT - 1) / NT;
-  __shared__ cplx<T> su[ZERO ? 1 : UY * UX];
-  __shared__ cplx<T> sr[RY * RX];   // f, then r
-  __shared__ cplx<T> sia[RY * RX];  // sigma, then 1/a
+  __shared__ cplx<TS> su[ZERO ? 1 : UY * UX];
+  __shared__ cplx<T> sr[RY * RX];     // f, then r (fp64)
+  __shared__ cplx<TS> sia[RY * RX];   // 1/a
+  __shared__ cplx<TS> ssg[ZERO ? 1 : RY * RX];
   __shared__ cplx<T> syc[YY * YX];
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  const T e = (T)W::Le * ih2;
+  const T e = W::Le * ih2;
   const cplx<T> zero = mkc<T>(0, 0);
+  const cplx<TS> zs = mkc<TS>(0, 0);
   // phase 1: every global load of the block, issued back to back
   if (!ZERO) {
 #pragma unroll
@@ -128,7 +153,7 @@ __global__ void __launch_bounds__(256) k_smooth_rb2d_fine(Geo g, const cplx<TS> 
       const int i = tid + k * NT;
       if (i < UY * UX) {
         const int gx = x0 - 3 + i % UX, gy = y0 - 3 + i / UX;
-        su[i] = g.inside(gx, gy, 0) ? u[g.idx(gx, gy, 0)] : zero;
+        su[i] = g.inside(gx, gy, 0) ? u[g.idx(gx, gy, 0)] : zs;
       }
     }
   }
@@ -139,55 +164,49 @@ __global__ void __launch_bounds__(256) k_smooth_rb2d_fine(Geo g, const cplx<TS> 
       const int gx = x0 - 2 + i % RX, gy = y0 - 2 + i / RX;
       const bool in = g.inside(gx, gy, 0);
       const int64_t j = g.idx(gx, gy, 0);
-      sr[i] = in ? f[j] : zero;
-      sia[i] = in ? sig[j] : zero;
+      sr[i] = in ? ccast<T, TS>(f[j]) : zero;
+      sia[i] = in ? ia[j] : zs;
+      if (!ZERO) ssg[i] = in ? sig[j] : zs;
     }
   }
   __syncthreads();
-  // phase 2: r = f - H_s u and 1/a on the tile + 2 (in place)
+  // phase 2: r = f - H_s u on the tile + 2 (fp64)
+  if (!ZERO) {
 #pragma unroll
-  for (int k = 0; k < NR; ++k) {
-    const int i = tid + k * NT;
-    if (i >= RY * RX) continue;
-    const int lx = i % RX, ly = i / RX;
-    if (!g.inside(x0 - 2 + lx, y0 - 2 + ly, 0)) { sia[i] = zero; continue; }
-    cplx<T> ss = sia[i];
-    ss.y = fma(-alpha, ss.x, ss.y);
-    const cplx<T> a = mkc<T>((T)W::Lc * ih2 - (T)W::Mc * ss.x, -(T)W::Mc * ss.y);
-    if (!ZERO) {
-      using Q = double;   // fp64 residual
-      auto U = [&](int k) { return ccast<Q, T>(su[(ly + 1) * UX + (lx + 1) + k]); };
-      const cplx<Q> uc = U(0);
-      const cplx<Q> sf = cadd<Q>(cadd<Q>(U(-1), U(1)), cadd<Q>(U(-UX), U(UX)));
-      cplx<Q> Lx = cscale<Q>(uc, (Q)W::Lc);
-      Lx = cfmar<Q>(Lx, (Q)W::Lf, sf);
+    for (int k = 0; k < NR; ++k) {
+      const int i = tid + k * NT;
+      if (i >= RY * RX) continue;
+      const int lx = i % RX, ly = i / RX;
+      if (!g.inside(x0 - 2 + lx, y0 - 2 + ly, 0)) continue;
+      auto U = [&](int o) { return ccast<T, TS>(su[(ly + 1) * UX + (lx + 1) + o]); };
+      const cplx<T> uc = U(0);
+      const cplx<T> sf = cadd<T>(cadd<T>(U(-1), U(1)), cadd<T>(U(-UX), U(UX)));
+      cplx<T> Lx = cscale<T>(uc, (T)W::Lc);
+      Lx = cfmar<T>(Lx, (T)W::Lf, sf);
       if (W::Le != 0.0) {
-        const cplx<Q> se = cadd<Q>(cadd<Q>(U(-UX - 1), U(-UX + 1)), cadd<Q>(U(UX - 1), U(UX + 1)));
-        Lx = cfmar<Q>(Lx, (Q)W::Le, se);
+        const cplx<T> se = cadd<T>(cadd<T>(U(-UX - 1), U(-UX + 1)), cadd<T>(U(UX - 1), U(UX + 1)));
+        Lx = cfmar<T>(Lx, (T)W::Le, se);
       }
-      Lx = cscale<Q>(Lx, ih2_d);
-      cplx<Q> Mx = cscale<Q>(uc, (Q)W::Mc);
-      if (W::Mf != 0.0) Mx = cfmar<Q>(Mx, (Q)W::Mf, sf);
-      cplx<Q> sq = ccast<Q, T>(sia[i]);
-      sq.y = fma(-alpha_d, sq.x, sq.y);
-      sr[i] = ccast<T, Q>(csub<Q>(ccast<Q, T>(sr[i]), csub<Q>(Lx, cmul<Q>(sq, Mx))));
+      Lx = cscale<T>(Lx, ih2);
+      cplx<T> Mx = cscale<T>(uc, (T)W::Mc);
+      if (W::Mf != 0.0) Mx = cfmar<T>(Mx, (T)W::Mf, sf);
+      cplx<T> ss = ccast<T, TS>(ssg[i]);
+      ss.y = fma(-alpha, ss.x, ss.y);
+      sr[i] = csub<T>(sr[i], csub<T>(Lx, cmul<T>(ss, Mx)));
     }
-    sia[i] = crecip_fast<T>(a);
+    __syncthreads();
   }
-  __syncthreads();
   // phase 3: centre solutions of the patches anchored on the tile + 1
   for (int i = tid; i < YY * YX; i += NT) {
     const int lx = i % YX, ly = i / YX;
-    if (!g.inside(x0 - 1 + lx, y0 - 1 + ly, 0)) { syc[i] = zero; continue; }
+    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+    if (!g.inside(gx, gy, 0)) { syc[i] = zero; continue; }
     const int ri = (ly + 1) * RX + (lx + 1);
     // clipped leaves sit outside the domain, where sr = sia = 0: they drop out
-    const cplx<T> s_r = cadd<T>(cadd<T>(cmul<T>(sr[ri - RX - 1], sia[ri - RX - 1]), cmul<T>(sr[ri - RX + 1], sia[ri - RX + 1])),
-                                cadd<T>(cmul<T>(sr[ri + RX - 1], sia[ri + RX - 1]), cmul<T>(sr[ri + RX + 1], sia[ri + RX + 1])));
-    const cplx<T> s_i = cadd<T>(cadd<T>(sia[ri - RX - 1], sia[ri - RX + 1]), cadd<T>(sia[ri + RX - 1], sia[ri + RX + 1]));
-    const cplx<T> ac = crecip_fast<T>(sia[ri]);
+    auto RL = [&](int o) { return cmul<T>(sr[ri + o], ccast<T, TS>(sia[ri + o])); };
+    const cplx<T> s_r = cadd<T>(cadd<T>(RL(-RX - 1), RL(-RX + 1)), cadd<T>(RL(RX - 1), RL(RX + 1)));
     const cplx<T> num = mkc<T>(sr[ri].x - e * s_r.x, sr[ri].y - e * s_r.y);
-    const cplx<T> den = mkc<T>(ac.x - e * e * s_i.x, ac.y - e * e * s_i.y);
-    syc[i] = cdiv_fast<T>(num, den);
+    syc[i] = cmul<T>(num, ccast<T, TS>(id[g.idx(gx, gy, 0)]));
   }
   __syncthreads();
   // phase 4: gather and write
@@ -208,11 +227,10 @@ __global__ void __launch_bounds__(256) k_smooth_rb2d_fine(Geo g, const cplx<TS> 
       }
       const int ri = (oy + 2) * RX + (ox + 2);
       const cplx<T> rj = sr[ri];
-      const cplx<T> lv = cmul<T>(mkc<T>((T)k * rj.x - e * syl.x, (T)k * rj.y - e * syl.y), sia[ri]);
-      const cplx<T> acc = cadd<T>(syc[yi], lv);
-      const cplx<T> upd = cscale<T>(acc, w / (T)(1 + k));
+      const cplx<T> lv = cmul<T>(mkc<T>((T)k * rj.x - e * syl.x, (T)k * rj.y - e * syl.y), ccast<T, TS>(sia[ri]));
+      const cplx<T> upd = cscale<T>(cadd<T>(syc[yi], lv), w / (T)(1 + k));
       const int64_t j = g.idx(gx, gy, 0);
-      u[j] = ZERO ? upd : cadd<T>(su[(oy + 3) * UX + (ox + 3)], upd);
+      u[j] = ccast<TS, T>(ZERO ? upd : cadd<T>(ccast<T, TS>(su[(oy + 3) * UX + (ox + 3)]), upd));
     }
   }
 }

@@ -3,8 +3,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/hmg.h"
 #include "common.cuh"
@@ -49,6 +51,26 @@ int krylov_multidot(int nv, bool self, const cplx<TV> *V, int64_t vstride, const
 template <typename TV, typename TW>
 int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef, double sgn, cplx<TW> *w, int64_t len,
                 double2 *partial_norm, cudaStream_t s);
+
+// Communication of the slab-partitioned solve (comm.cu).  All calls are
+// collective over the ranks and stream-ordered on `s`.
+struct Comm {
+  int rank = 0, size = 1;
+  virtual ~Comm() = default;
+  // send `bytes` from send_lo to rank-1 and from send_hi to rank+1; receive
+  // the matching blocks into recv_lo (from rank-1) and recv_hi (from rank+1)
+  virtual void halo(const void *send_lo, void *recv_lo, const void *send_hi, void *recv_hi, size_t bytes,
+                    cudaStream_t s) = 0;
+  virtual void allreduce_sum(double *d, int n, cudaStream_t s) = 0;   // in place, device fp64
+  // rank q owns bytes [off[q], off[q] + len[q]) of buf (same layout on every
+  // rank); afterwards every rank holds all of them
+  virtual void allgatherv(void *buf, const std::vector<size_t> &off, const std::vector<size_t> &len,
+                          cudaStream_t s) = 0;
+};
+std::shared_ptr<void> local_group_create(int n);
+Comm *local_comm_create(const std::shared_ptr<void> &group, int rank);
+void nccl_unique_id(void *out128);
+Comm *nccl_comm_create(const void *uid, int rank, int n);
 
 // Fused Galerkin-level Vanka sweep, 2D (smooth2d.cu).
 // hinv == nullptr: patches factored on the fly in every sweep; else the
