@@ -77,6 +77,14 @@ _sigs = {
     "hmg_profile_begin": ([], None),
     "hmg_profile_report": ([], ctypes.c_char_p),
     "hmg_hierarchy_destroy": ([_vp], None),
+    "hmg_comm_local_group": ([_i, ctypes.POINTER(_vp)], _i),
+    "hmg_comm_local_rank": ([_vp, _i, ctypes.POINTER(_vp)], _i),
+    "hmg_comm_nccl_unique_id": ([_vp], _i),
+    "hmg_comm_nccl": ([_vp, _i, _i, ctypes.POINTER(_vp)], _i),
+    "hmg_comm_destroy": ([_vp], None),
+    "hmg_build_hierarchy_dist": ([ctypes.POINTER(_Options), _vp, _d, _vp, _d, _vp, _vp, ctypes.POINTER(_vp)], _i),
+    "hmg_level_rows": ([_vp, _i, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i),
+    "hmg_slab_partition": ([_i64, _i, _i, _i, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i)], _i),
     "hmg_last_error": ([], ctypes.c_char_p),
     "hmg_version": ([], ctypes.c_char_p),
 }
@@ -140,6 +148,63 @@ def _ptr(t, dtype, n):
     return ctypes.c_void_p(t.data_ptr())
 
 
+class Comm:
+    """A rank's communicator (hmg_comm).  Build with ``LocalGroup(k).rank(r)``
+    (k virtual ranks on one GPU, one host thread each) or ``Comm.nccl(uid, rank, n)``."""
+
+    def __init__(self, handle, rank, size, keep=None):
+        self._h, self.rank, self.size, self._keep = handle, rank, size, keep
+
+    @staticmethod
+    def nccl_unique_id():
+        buf = (ctypes.c_char * 128)()
+        _check(_lib.hmg_comm_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, uid, rank, size):
+        buf = (ctypes.c_char * 128).from_buffer_copy(uid)
+        h = ctypes.c_void_p()
+        _check(_lib.hmg_comm_nccl(ctypes.cast(buf, ctypes.c_void_p), rank, size, ctypes.byref(h)))
+        return cls(h, rank, size)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.hmg_comm_destroy(self._h)
+            self._h = None
+
+
+class LocalGroup:
+    """k virtual ranks on the current GPU (hmg_comm_local_group)."""
+
+    def __init__(self, size):
+        h = ctypes.c_void_p()
+        _check(_lib.hmg_comm_local_group(size, ctypes.byref(h)))
+        self._h, self.size = h, size
+
+    def rank(self, r):
+        h = ctypes.c_void_p()
+        _check(_lib.hmg_comm_local_rank(self._h, r, ctypes.byref(h)))
+        return Comm(h, r, self.size, keep=self)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.hmg_comm_destroy(self._h)
+            self._h = None
+
+
+def slab_partition(nodes0, levels, nranks, ghost=4):
+    """Host-only partition rule (hmg_slab_partition): (lo, hi) arrays [levels, nranks], dist [levels]."""
+    lo = (ctypes.c_int64 * (levels * nranks))()
+    hi = (ctypes.c_int64 * (levels * nranks))()
+    dist = (ctypes.c_int * levels)()
+    n = _lib.hmg_slab_partition(nodes0, levels, nranks, ghost, lo, hi, dist)
+    if n < 0:
+        raise HmgError(EINVAL, "bad partition arguments")
+    return (np.array(lo[:]).reshape(levels, nranks), np.array(hi[:]).reshape(levels, nranks),
+            np.array(dist[:]))
+
+
 @dataclass
 class Report:
     iterations: int
@@ -173,7 +238,7 @@ class Options:
 class Hierarchy:
     """Owns an hmg_hierarchy handle (hmg_build_hierarchy ... hmg_hierarchy_destroy)."""
 
-    def __init__(self, opts: Options, kappa, omega, gamma, alpha, stream=None):
+    def __init__(self, opts: Options, kappa, omega, gamma, alpha, stream=None, comm: "Comm" = None):
         import torch
         o = _Options()
         o.dim = opts.dim
@@ -201,9 +266,15 @@ class Hierarchy:
             raise ValueError("kappa/gamma size does not match the grid")
         h = ctypes.c_void_p()
         self._h = None
-        _check(_lib.hmg_build_hierarchy(ctypes.byref(o), k.ctypes.data_as(ctypes.c_void_p), float(omega),
-                                        g.ctypes.data_as(ctypes.c_void_p), float(alpha), _stream(stream),
-                                        ctypes.byref(h)))
+        self.comm = comm
+        if comm is None:
+            _check(_lib.hmg_build_hierarchy(ctypes.byref(o), k.ctypes.data_as(ctypes.c_void_p), float(omega),
+                                            g.ctypes.data_as(ctypes.c_void_p), float(alpha), _stream(stream),
+                                            ctypes.byref(h)))
+        else:
+            _check(_lib.hmg_build_hierarchy_dist(ctypes.byref(o), k.ctypes.data_as(ctypes.c_void_p), float(omega),
+                                                 g.ctypes.data_as(ctypes.c_void_p), float(alpha), comm._h,
+                                                 _stream(stream), ctypes.byref(h)))
         self._h = h
         self.levels = int(_lib.hmg_num_levels(h))
 
@@ -219,6 +290,13 @@ class Hierarchy:
         if N < 0:
             raise HmgError(EINVAL, "level out of range")
         return int(N), tuple(int(n[a]) for a in range(self.opts.dim))
+
+    def level_rows(self, level):
+        """Global slab-axis rows [lo, hi) this rank holds on ``level``."""
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        if _lib.hmg_level_rows(self._h, level, ctypes.byref(lo), ctypes.byref(hi)) != 0:
+            raise HmgError(EINVAL, "level out of range")
+        return lo.value, hi.value
 
     def stencil_radius(self, level):
         return int(_lib.hmg_stencil_radius(self._h, level))

@@ -1,6 +1,3 @@
 set -x
-python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_exit=$? >> gpurun_out/bench.err
-CMD="python bench.py --n 2048 --steps 1 --warmup 1 --no-cpu-baseline"
-timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_smooth_stored2d|k_smooth_rb2d_fine|k_multidot|k_multi_axpy" -s 0 -c 14 -o gpurun_out/prof_r1 $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu_full_exit=$? >> gpurun_out/ncu_full.log
+timeout 900 python -m pytest tests/test_gpu_multirank.py -q -p no:cacheprovider -x > gpurun_out/gpu_multirank.log 2>&1; echo exit=$? >> gpurun_out/gpu_multirank.log
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
