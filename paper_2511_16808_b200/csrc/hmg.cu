@@ -626,23 +626,24 @@ template <typename T> struct Solver : SolverBase {
     else restrict_t<D>(l, (const D *)r, (D *)fc, s);
   }
 
-  template <typename TU> void prolong_t(int l, const D *e, TU *u, cudaStream_t s) {
+  template <typename TU> void prolong_t(int l, const D *e, const TU *u, TU *uo, cudaStream_t s) {
     const Level &F = lev[l], &Cc = lev[l + 1];
     halo(l + 1, e, 1, s);
     auto nl = node_launch(F.geo);
     using BU = decltype(u->x);
     tag("prolong_add", l, 2.0 * sizeof(TU) * F.geo.nodes() + (double)sizeof(D) * Cc.geo.nodes());
     if (opt.dim == 2) {
-      if (F.rP == 1) launch(k_prolong_add<double, BU, 2, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u);
-      else launch(k_prolong_add<double, BU, 2, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u);
+      if (F.rP == 1) launch(k_prolong_add<double, BU, 2, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u, uo);
+      else launch(k_prolong_add<double, BU, 2, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u, uo);
     } else {
-      if (F.rP == 1) launch(k_prolong_add<double, BU, 3, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u);
-      else launch(k_prolong_add<double, BU, 3, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u);
+      if (F.rP == 1) launch(k_prolong_add<double, BU, 3, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u, uo);
+      else launch(k_prolong_add<double, BU, 3, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u, uo);
     }
   }
-  void prolong_(int l, const void *e, void *u, cudaStream_t s) {
-    if (l == 0) prolong_t<C>(l, (const D *)e, (C *)u, s);
-    else prolong_t<D>(l, (const D *)e, (D *)u, s);
+  // u_out = u + P_l e  (u_out may be u)
+  void prolong_(int l, const void *e, const void *u, void *u_out, cudaStream_t s) {
+    if (l == 0) prolong_t<C>(l, (const D *)e, (const C *)u, (C *)u_out, s);
+    else prolong_t<D>(l, (const D *)e, (const D *)u, (D *)u_out, s);
   }
 
   // generic two-pass Vanka (stored patch inverses + gather); TV = level vector type
@@ -671,30 +672,38 @@ template <typename T> struct Solver : SolverBase {
     }
   }
 
-  // one additive Vanka relaxation u <- u + w B (f - A u) (Eq. 3.8); zero: u == 0 on input
-  void smooth(int l, const void *f, void *u, int zero, cudaStream_t s) {
+  // Do the level's sweeps read neighbours of u inside one kernel?  Then they
+  // must run out of place (other blocks may still read the old u).
+  bool fused_sweep(int l) const { return (l == 0 && rb_closed) || fused_level(l); }
+
+  // one additive Vanka relaxation (Eq. 3.8): u_out = u + w B (f - A u);
+  // zero: u == 0 (u may be null).  Fused levels: u_out != u required;
+  // generic levels: in place (u_out == u).
+  void smooth(int l, const void *f, const void *u, void *u_out, int zero, cudaStream_t s) {
     Level &Lv = lev[l];
     const double w = damp(l);
     const double nn = (double)Lv.geo.nodes();
     if (l == 0 && rb_closed) {
-      // fused sweep: residual (unless zero), closed-form patch solves, gather; fp64 arithmetic
+      // warp-marching fused sweep: residual (unless zero), closed-form patch solves, gather; fp64 arithmetic
       const double ih2 = 1.0 / (Lv.h * Lv.h);
-      constexpr int TX = 32, TY = sizeof(T) == 8 ? 8 : 16;   // fp64 storage: 32 x 8 tiles keep smem < 48 KB
-      dim3 grid((Lv.geo.n[0] + TX - 1) / TX, (Lv.geo.n[1] + TY - 1) / TY), block(32, 8);
+      constexpr int SEG = 32;   // output rows per warp segment (4 pipeline rows of overlap)
+      const int nstrips = (Lv.geo.n[0] + RB_STRIP - 1) / RB_STRIP, nsegs = (Lv.geo.n[1] + SEG - 1) / SEG;
+      const int64_t warps = (int64_t)nstrips * nsegs;
+      const dim3 grid((unsigned)((warps + 7) / 8)), block(256);
       const C *sg = sig.template as<C>();
       const C *ia = rb_ia.template as<C>(), *id = rb_id.template as<C>();
-      const C *ff = (const C *)f;
-      C *uu = (C *)u;
+      const C *ff = (const C *)f, *ui = (const C *)u;
+      C *uo = (C *)u_out;
       if (!zero) halo(0, u, 3, s);
       halo(0, f, 2, s);
       tag(zero ? "smooth_rb2d_fine_zero" : "smooth_rb2d_fine", 0, (zero ? 4 : 6) * sizeof(C) * nn);
       const bool c4 = opt.fine_stencil == HMG_COMPACT4;
       if (zero) {
-        if (c4) launch(k_smooth_rb2d_fine<T, ST_COMPACT4, TX, TY, true>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, uu, w);
-        else launch(k_smooth_rb2d_fine<T, ST_FD2, TX, TY, true>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, uu, w);
+        if (c4) launch(k_rb2d_march<T, ST_COMPACT4, true, SEG>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        else launch(k_rb2d_march<T, ST_FD2, true, SEG>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
       } else {
-        if (c4) launch(k_smooth_rb2d_fine<T, ST_COMPACT4, TX, TY, false>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, uu, w);
-        else launch(k_smooth_rb2d_fine<T, ST_FD2, TX, TY, false>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, uu, w);
+        if (c4) launch(k_rb2d_march<T, ST_COMPACT4, false, SEG>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        else launch(k_rb2d_march<T, ST_FD2, false, SEG>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
       }
       return;
     }
@@ -708,16 +717,27 @@ template <typename T> struct Solver : SolverBase {
           ((Lv.hinv.p ? (zero ? 0.0 : kcount(opt.dim, Lv.r)) : planes) + hplanes) * sizeof(C) * nn +
               (zero ? 2 : 3) * sizeof(D) * nn);
       smooth_stored2d<T>(Lv.r, opt.smoother, zero != 0, Lv.geo, (const C *)Lv.coef.template as<C>(),
-                         (const C *)Lv.hinv.template as<C>(), (const D *)f, (D *)u, w, s);
+                         (const C *)Lv.hinv.template as<C>(), (const D *)f, (const D *)u, (D *)u_out, w, s);
       return;
     }
+    if (u_out != u && !zero) CK(cudaMemcpyAsync(u_out, u, Lv.geo.total * vsize(l), cudaMemcpyDeviceToDevice, s));
     const void *r = f;
     if (!zero) {
-      op(l, 1, u, f, Lv.r_.p, s);
+      op(l, 1, u_out, f, Lv.r_.p, s);
       r = Lv.r_.p;
     }
-    if (l == 0) vanka_kind<C>(l, r, u, zero, s);
-    else vanka_kind<D>(l, r, u, zero, s);
+    if (l == 0) vanka_kind<C>(l, r, u_out, zero, s);
+    else vanka_kind<D>(l, r, u_out, zero, s);
+  }
+  // in-place sweep on any level (fused levels go through the r_ scratch)
+  void smooth_inplace(int l, const void *f, void *u, cudaStream_t s) {
+    if (!fused_sweep(l)) {
+      smooth(l, f, u, u, 0, s);
+      return;
+    }
+    void *S = lev[l].r_.p;
+    smooth(l, f, u, S, 0, s);
+    CK(cudaMemcpyAsync(u, S, lev[l].geo.total * vsize(l), cudaMemcpyDeviceToDevice, s));
   }
 
   void coarse_(const void *r, void *e, cudaStream_t s) {
@@ -735,15 +755,24 @@ template <typename T> struct Solver : SolverBase {
       return;
     }
     Level &Lv = lev[l];
-    for (int k = 0; k < opt.nu1; ++k) smooth(l, f, u, zero && k == 0, s);
+    for (int k = 0; k < opt.nu1; ++k) {                        // step 1: pre-smoothing
+      if (k == 0 && zero) smooth(l, f, nullptr, u, 1, s);      //   zero guess: r = f, u written only
+      else smooth_inplace(l, f, u, s);
+    }
     if (opt.nu1 == 0 && zero) CK(cudaMemsetAsync(u, 0, Lv.geo.total * vsize(l), s));
     op(l, 1, u, f, Lv.r_.p, s);                                // step 2: r = f - A u
     Level &Cc = lev[l + 1];
     restrict_(l, Lv.r_.p, Cc.f.p, s);                          //         f_c = R r
     const int rec = opt.cycle == 1 ? 2 : 1;                    // step 3: V / W recursion
     for (int c = 0; c < rec; ++c) cycle(l + 1, Cc.f.p, Cc.u.p, c == 0, s);
-    prolong_(l, Cc.u.p, u, s);                                 // step 4: u += P e
-    for (int k = 0; k < opt.nu2; ++k) smooth(l, f, u, 0, s);   // step 5
+    if (opt.nu2 > 0 && fused_sweep(l)) {
+      prolong_(l, Cc.u.p, u, Lv.r_.p, s);                      // step 4: S = u + P e (r_ is free now)
+      smooth(l, f, Lv.r_.p, u, 0, s);                          // step 5: u = S + w B (f - A S)
+      for (int k = 1; k < opt.nu2; ++k) smooth_inplace(l, f, u, s);
+    } else {
+      prolong_(l, Cc.u.p, u, u, s);                            // step 4: u += P e
+      for (int k = 0; k < opt.nu2; ++k) smooth_inplace(l, f, u, s);   // step 5
+    }
   }
 
   // ------------------------------------------------------------ API glue
@@ -786,7 +815,7 @@ template <typename T> struct Solver : SolverBase {
     Level &Lv = lev[l];
     pack(l, f, Lv.f.p, s);
     pack(l, u, Lv.u.p, s);
-    smooth(l, Lv.f.p, Lv.u.p, 0, s);
+    smooth_inplace(l, Lv.f.p, Lv.u.p, s);
     unpack(l, Lv.u.p, u, s);
   }
   void api_restrict(int l, const void *r, void *fc, cudaStream_t s) override {
@@ -799,7 +828,7 @@ template <typename T> struct Solver : SolverBase {
     check_level(l, false);
     pack(l + 1, ec, lev[l + 1].u.p, s);
     pack(l, u, lev[l].u.p, s);
-    prolong_(l, lev[l + 1].u.p, lev[l].u.p, s);
+    prolong_(l, lev[l + 1].u.p, lev[l].u.p, lev[l].u.p, s);
     unpack(l, lev[l].u.p, u, s);
   }
   void api_coarse(const void *r, void *e, cudaStream_t s) override {

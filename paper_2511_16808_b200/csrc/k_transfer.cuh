@@ -71,9 +71,10 @@ __device__ __forceinline__ int prolong_taps(int i, int *J, double *w) {
   return 2;
 }
 
+// u_out = u + P e (u_out may equal u: each node reads and writes only itself)
 template <typename TE, typename TU, int DIM, int PR>
 __global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<TE> *__restrict__ e,
-                                                     cplx<TU> *__restrict__ u) {
+                                                     const cplx<TU> *u, cplx<TU> *u_out) {
   using T = double;
   HMG_NODE_IDX(gf, ix, iy, iz);
   int Jx[3], Jy[3], Jz[3];
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<
     acc = cfmar<T>(acc, (T)wz[c], accy);
   }
   const int64_t i = gf.idx(ix, iy, iz);
-  u[i] = ccast<TU, T>(cadd<T>(ccast<T, TU>(u[i]), acc));
+  u_out[i] = ccast<TU, T>(cadd<T>(ccast<T, TU>(u[i]), acc));
 }
 
 }  // namespace hmg

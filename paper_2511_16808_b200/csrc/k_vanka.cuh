@@ -125,112 +125,117 @@ __global__ void k_rb_factors(Geo g, const double2 *__restrict__ sigd, double alp
   id[j] = ccast<TS, double>(crecip<double>(make_double2(ac.x - e * e * si.x, ac.y - e * e * si.y)));
 }
 
-template <typename TS, int KIND, int TX, int TY, bool ZERO>
-__global__ void __launch_bounds__(256) k_smooth_rb2d_fine(Geo g, const cplx<TS> *__restrict__ sig,
-                                                          const cplx<TS> *__restrict__ ia,
-                                                          const cplx<TS> *__restrict__ id, double alpha, double ih2,
-                                                          const cplx<TS> *__restrict__ f, cplx<TS> *__restrict__ u,
-                                                          double w) {
+// (1b') the same RB sweep as a WARP-MARCHING stencil: each warp owns a strip
+// of 32 columns (26 outputs: 3 halo lanes per side, the reach of u -> r ->
+// y_c -> u) and marches along y through a segment of SEG output rows, holding
+// a rolling window of rows in registers; x-neighbours come from warp shuffles.
+// No shared memory, no barriers; every array is streamed once per row (x 32/26).
+// Pipeline at step b (row b of r):  load u(b+1), f(b), sigma(b), ia(b), id(b-1);
+//   r(b) = f - H_s u (fp64) and t(b) = r ia;  y_c(b-1) = (r - e sum_diag t) id;
+//   output row b-2 = u + w/cnt (y_c + (k r - e sum_diag y_c) ia).
+__device__ __forceinline__ double2 shfl_up1(double2 v) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ double2 shfl_dn1(double2 v) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+
+constexpr int RB_STRIP = 26;
+
+// Out of place: u_out = u_in + w B (f - H_s u_in) (u_in unused with ZERO).  In
+// place would race: other warps still read old u in their halo rows/columns.
+template <typename TS, int KIND, bool ZERO, int SEG>
+__global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__restrict__ sig,
+                                                    const cplx<TS> *__restrict__ ia_, const cplx<TS> *__restrict__ id_,
+                                                    double alpha, double ih2, const cplx<TS> *__restrict__ f,
+                                                    const cplx<TS> *__restrict__ u, cplx<TS> *__restrict__ u_out,
+                                                    double w) {
   using W = FineW<2, KIND>;
-  using T = double;
-  constexpr int NT = 256;
-  constexpr int UX = TX + 6, UY = TY + 6, RX = TX + 4, RY = TY + 4, YX = TX + 2, YY = TY + 2;
-  constexpr int NU = (UX * UY + NT - 1) / NT, NR = (RX * RY + NT - 1) / NT;
-  __shared__ cplx<TS> su[ZERO ? 1 : UY * UX];
-  __shared__ cplx<T> sr[RY * RX];     // f, then r (fp64)
-  __shared__ cplx<TS> sia[RY * RX];   // 1/a
-  __shared__ cplx<TS> ssg[ZERO ? 1 : RY * RX];
-  __shared__ cplx<T> syc[YY * YX];
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  const T e = W::Le * ih2;
-  const cplx<T> zero = mkc<T>(0, 0);
-  const cplx<TS> zs = mkc<TS>(0, 0);
-  // phase 1: every global load of the block, issued back to back
+  using D = double;
+  using CD = cplx<D>;
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nstrips = (g.n[0] + RB_STRIP - 1) / RB_STRIP;
+  const int strip = wid % nstrips, seg = wid / nstrips;
+  const int y0 = seg * SEG;
+  if (y0 >= g.n[1]) return;
+  const int y1 = min(g.n[1], y0 + SEG);
+  const int x = strip * RB_STRIP - 3 + lane;
+  const bool out_lane = lane >= 3 && lane < 3 + RB_STRIP && x < g.n[0];
+  const D e = W::Le * ih2;
+  const CD z = mkc<D>(0, 0);
+  auto in = [&](int y) { return g.inside(x, y, 0); };
+  // rolling window
+  CD um1 = z, u0 = z, up1 = z;          // u at rows b-1, b, b+1
+  CD ub1 = z;                           // u at row b-2 (the output row)
+  CD r2 = z, r1 = z, r0 = z;            // r at rows b-2, b-1, b
+  CD t2 = z, t1 = z, t0 = z;            // t = r ia at rows b-2, b-1, b
+  CD a2 = z, a1 = z, a0 = z;            // ia at rows b-2, b-1, b
+  CD c3 = z, c2 = z, c1 = z;            // y_c at rows b-3, b-2, b-1
+  // one-step-ahead prefetch registers, kept in the storage type so that the
+  // loads of step b+1 stay in flight during step b
+  using CS = cplx<TS>;
+  const CS zs = mkc<TS>(0, 0);
+  auto lr = [&](const CS *a, int y) { return in(y) ? a[g.idx(x, y, 0)] : zs; };
   if (!ZERO) {
-#pragma unroll
-    for (int k = 0; k < NU; ++k) {
-      const int i = tid + k * NT;
-      if (i < UY * UX) {
-        const int gx = x0 - 3 + i % UX, gy = y0 - 3 + i / UX;
-        su[i] = g.inside(gx, gy, 0) ? u[g.idx(gx, gy, 0)] : zs;
-      }
+    u0 = ccast<D, TS>(lr(u, y0 - 3));
+    up1 = ccast<D, TS>(lr(u, y0 - 2));
+  }
+  CS pu = ZERO ? zs : lr(u, y0 - 1), pf = lr(f, y0 - 2), pa = lr(ia_, y0 - 2), pid = lr(id_, y0 - 3);
+  CS ps = ZERO ? zs : lr(sig, y0 - 2);
+  for (int b = y0 - 2; b <= y1 + 1; ++b) {
+    if (!ZERO) {
+      ub1 = um1;
+      um1 = u0; u0 = up1; up1 = ccast<D, TS>(pu);
+      pu = lr(u, b + 2);
     }
-  }
-#pragma unroll
-  for (int k = 0; k < NR; ++k) {
-    const int i = tid + k * NT;
-    if (i < RY * RX) {
-      const int gx = x0 - 2 + i % RX, gy = y0 - 2 + i / RX;
-      const bool in = g.inside(gx, gy, 0);
-      const int64_t j = g.idx(gx, gy, 0);
-      sr[i] = in ? ccast<T, TS>(f[j]) : zero;
-      sia[i] = in ? ia[j] : zs;
-      if (!ZERO) ssg[i] = in ? sig[j] : zs;
+    const CD fb = ccast<D, TS>(pf), ab = ccast<D, TS>(pa), idb = ccast<D, TS>(pid);
+    CD sb = ccast<D, TS>(ps);
+    pf = lr(f, b + 1);
+    pa = lr(ia_, b + 1);
+    pid = lr(id_, b);
+    if (!ZERO) ps = lr(sig, b + 1);
+    // ---- r(b), t(b)  (fp64)
+    CD rb = fb;
+    if (!ZERO) {
+      const CD ul = shfl_up1(u0), ur = shfl_dn1(u0);
+      const CD uml = shfl_up1(um1), umr = shfl_dn1(um1), upl = shfl_up1(up1), upr = shfl_dn1(up1);
+      const CD sf = cadd<D>(cadd<D>(ul, ur), cadd<D>(um1, up1));
+      CD Lx = cscale<D>(u0, (D)W::Lc);
+      Lx = cfmar<D>(Lx, (D)W::Lf, sf);
+      if (W::Le != 0.0) Lx = cfmar<D>(Lx, (D)W::Le, cadd<D>(cadd<D>(uml, umr), cadd<D>(upl, upr)));
+      Lx = cscale<D>(Lx, ih2);
+      CD Mx = cscale<D>(u0, (D)W::Mc);
+      if (W::Mf != 0.0) Mx = cfmar<D>(Mx, (D)W::Mf, sf);
+      sb.y = fma(-alpha, sb.x, sb.y);
+      rb = in(b) ? csub<D>(fb, csub<D>(Lx, cmul<D>(sb, Mx))) : z;
     }
-  }
-  __syncthreads();
-  // phase 2: r = f - H_s u on the tile + 2 (fp64)
-  if (!ZERO) {
-#pragma unroll
-    for (int k = 0; k < NR; ++k) {
-      const int i = tid + k * NT;
-      if (i >= RY * RX) continue;
-      const int lx = i % RX, ly = i / RX;
-      if (!g.inside(x0 - 2 + lx, y0 - 2 + ly, 0)) continue;
-      auto U = [&](int o) { return ccast<T, TS>(su[(ly + 1) * UX + (lx + 1) + o]); };
-      const cplx<T> uc = U(0);
-      const cplx<T> sf = cadd<T>(cadd<T>(U(-1), U(1)), cadd<T>(U(-UX), U(UX)));
-      cplx<T> Lx = cscale<T>(uc, (T)W::Lc);
-      Lx = cfmar<T>(Lx, (T)W::Lf, sf);
-      if (W::Le != 0.0) {
-        const cplx<T> se = cadd<T>(cadd<T>(U(-UX - 1), U(-UX + 1)), cadd<T>(U(UX - 1), U(UX + 1)));
-        Lx = cfmar<T>(Lx, (T)W::Le, se);
-      }
-      Lx = cscale<T>(Lx, ih2);
-      cplx<T> Mx = cscale<T>(uc, (T)W::Mc);
-      if (W::Mf != 0.0) Mx = cfmar<T>(Mx, (T)W::Mf, sf);
-      cplx<T> ss = ccast<T, TS>(ssg[i]);
-      ss.y = fma(-alpha, ss.x, ss.y);
-      sr[i] = csub<T>(sr[i], csub<T>(Lx, cmul<T>(ss, Mx)));
+    r2 = r1; r1 = r0; r0 = rb;
+    a2 = a1; a1 = a0; a0 = ab;
+    t2 = t1; t1 = t0; t0 = cmul<D>(rb, ab);
+    // ---- y_c(b-1): diagonal leaves at rows b-2 and b, columns x +- 1
+    {
+      const CD sdiag = cadd<D>(cadd<D>(shfl_up1(t2), shfl_dn1(t2)), cadd<D>(shfl_up1(t0), shfl_dn1(t0)));
+      const CD num = mkc<D>(r1.x - e * sdiag.x, r1.y - e * sdiag.y);
+      const CD yc = in(b - 1) ? cmul<D>(num, idb) : z;
+      c3 = c2; c2 = c1; c1 = yc;
     }
-    __syncthreads();
-  }
-  // phase 3: centre solutions of the patches anchored on the tile + 1
-  for (int i = tid; i < YY * YX; i += NT) {
-    const int lx = i % YX, ly = i / YX;
-    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
-    if (!g.inside(gx, gy, 0)) { syc[i] = zero; continue; }
-    const int ri = (ly + 1) * RX + (lx + 1);
-    // clipped leaves sit outside the domain, where sr = sia = 0: they drop out
-    auto RL = [&](int o) { return cmul<T>(sr[ri + o], ccast<T, TS>(sia[ri + o])); };
-    const cplx<T> s_r = cadd<T>(cadd<T>(RL(-RX - 1), RL(-RX + 1)), cadd<T>(RL(RX - 1), RL(RX + 1)));
-    const cplx<T> num = mkc<T>(sr[ri].x - e * s_r.x, sr[ri].y - e * s_r.y);
-    syc[i] = cmul<T>(num, ccast<T, TS>(id[g.idx(gx, gy, 0)]));
-  }
-  __syncthreads();
-  // phase 4: gather and write
-  for (int oy = threadIdx.y; oy < TY; oy += blockDim.y) {
-    for (int ox = threadIdx.x; ox < TX; ox += blockDim.x) {
-      const int gx = x0 + ox, gy = y0 + oy;
-      if (!g.inside(gx, gy, 0)) continue;
-      const int yi = (oy + 1) * YX + (ox + 1);
-      cplx<T> syl = zero;
-      int k = 0;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const int dx = (s & 1) ? 1 : -1, dy = (s & 2) ? 1 : -1;
-        if (g.inside(gx - dx, gy - dy, 0)) {
-          syl = cadd<T>(syl, syc[yi - dy * YX - dx]);
-          ++k;
-        }
+    // ---- output row b-2
+    const int yo = b - 2;
+    if (yo >= y0 && yo < y1) {
+      const CD cl3 = shfl_up1(c3), cr3 = shfl_dn1(c3), cl1 = shfl_up1(c1), cr1 = shfl_dn1(c1);
+      if (out_lane && in(yo)) {
+        // anchors j - (dx, dy) for the 4 diagonal offsets: rows yo -+ 1, columns x -+ 1
+        CD syl = z;
+        int k = 0;
+        if (g.inside(x - 1, yo - 1, 0)) { syl = cadd<D>(syl, cl3); ++k; }
+        if (g.inside(x + 1, yo - 1, 0)) { syl = cadd<D>(syl, cr3); ++k; }
+        if (g.inside(x - 1, yo + 1, 0)) { syl = cadd<D>(syl, cl1); ++k; }
+        if (g.inside(x + 1, yo + 1, 0)) { syl = cadd<D>(syl, cr1); ++k; }
+        const CD lv = cmul<D>(mkc<D>((D)k * r2.x - e * syl.x, (D)k * r2.y - e * syl.y), a2);
+        const CD upd = cscale<D>(cadd<D>(c2, lv), w / (D)(1 + k));
+        u_out[g.idx(x, yo, 0)] = ccast<TS, D>(ZERO ? upd : cadd<D>(ub1, upd));
       }
-      const int ri = (oy + 2) * RX + (ox + 2);
-      const cplx<T> rj = sr[ri];
-      const cplx<T> lv = cmul<T>(mkc<T>((T)k * rj.x - e * syl.x, (T)k * rj.y - e * syl.y), ccast<T, TS>(sia[ri]));
-      const cplx<T> upd = cscale<T>(cadd<T>(syc[yi], lv), w / (T)(1 + k));
-      const int64_t j = g.idx(gx, gy, 0);
-      u[j] = ccast<TS, T>(ZERO ? upd : cadd<T>(ccast<T, TS>(su[(oy + 3) * UX + (ox + 3)]), upd));
     }
   }
 }
@@ -288,11 +293,12 @@ __device__ __forceinline__ void small_solve(cplx<T> (&A)[K][K], cplx<T> (&b)[K])
 // in registers (no stored inverses), the K local values staged in shared
 // memory, then the 1/cnt-weighted gather.  HBM: the K stencil planes, u, f
 // read once, u written once (ZERO: f and the patch planes only).
+// Out of place: u_out = u + w B (f - A u) (u unused with ZERO).
 template <typename T, typename TK, int R, int KIND, int TX, int TY, bool ZERO, bool HINV>
 __global__ void __launch_bounds__(256, 2) k_smooth_stored2d(Geo g, const cplx<TK> *__restrict__ coef,
                                                          const cplx<TK> *__restrict__ hinv,
-                                                         const cplx<T> *__restrict__ f, cplx<T> *__restrict__ u,
-                                                         T w) {
+                                                         const cplx<T> *__restrict__ f, const cplx<T> *__restrict__ u,
+                                                         cplx<T> *__restrict__ u_out, T w) {
   using P = Patch<2, KIND>;
   constexpr int K = P::K;
   constexpr int NT = 256;
@@ -405,7 +411,7 @@ __global__ void __launch_bounds__(256, 2) k_smooth_stored2d(Geo g, const cplx<TK
       }
       const cplx<T> upd = cscale<T>(acc, w / (T)P::count(g, gx, gy, 0));
       const int64_t j = g.idx(gx, gy, 0);
-      u[j] = ZERO ? upd : cadd<T>(su[(oy + HU) * UX + (ox + HU)], upd);
+      u_out[j] = ZERO ? upd : cadd<T>(su[(oy + HU) * UX + (ox + HU)], upd);
     }
   }
 }

@@ -77,6 +77,6 @@ Comm *nccl_comm_create(const void *uid, int rank, int n);
 // stored patch inverses are applied.
 template <typename T>
 void smooth_stored2d(int r, int kind, bool zero, const Geo &g, const cplx<T> *coef, const cplx<T> *hinv,
-                     const double2 *f, double2 *u, double w, cudaStream_t s);
+                     const double2 *f, const double2 *u, double2 *u_out, double w, cudaStream_t s);
 
 }  // namespace hmg

@@ -8,45 +8,45 @@ namespace hmg {
 
 // vectors and arithmetic fp64 on every Galerkin level; coefficients TK
 template <typename TK, int R, int KIND>
-static void go(bool zero, const Geo &g, const cplx<TK> *coef, const cplx<TK> *hinv, const double2 *f, double2 *u,
-               double w, cudaStream_t s) {
+static void go(bool zero, const Geo &g, const cplx<TK> *coef, const cplx<TK> *hinv, const double2 *f,
+               const double2 *u, double2 *uo, double w, cudaStream_t s) {
   constexpr int TX = 32, TY = 8;   // fp64 tiles: 32 x 8 keeps static smem under 48 KB
   const dim3 grid((g.n[0] + TX - 1) / TX, (g.n[1] + TY - 1) / TY), block(32, 8);
   if (hinv) {
-    if (zero) launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, true, true>, grid, block, 0, s, g, coef, hinv, f, u, w);
-    else launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, false, true>, grid, block, 0, s, g, coef, hinv, f, u, w);
+    if (zero) launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, true, true>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
+    else launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, false, true>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
   } else {
-    if (zero) launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, true, false>, grid, block, 0, s, g, coef, hinv, f, u, w);
-    else launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, false, false>, grid, block, 0, s, g, coef, hinv, f, u, w);
+    if (zero) launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, true, false>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
+    else launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, false, false>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
   }
 }
 
 template <typename T, int R>
 static void go_kind(int kind, bool zero, const Geo &g, const cplx<T> *coef, const cplx<T> *hinv, const double2 *f,
-                    double2 *u, double w, cudaStream_t s) {
+                    const double2 *u, double2 *uo, double w, cudaStream_t s) {
   switch (kind) {
-    case HMG_VANKA_RB: go<T, R, PK_RB>(zero, g, coef, hinv, f, u, w, s); return;
-    case HMG_VANKA_ELEMENT: go<T, R, PK_ELEMENT>(zero, g, coef, hinv, f, u, w, s); return;
-    case HMG_JACOBI: go<T, R, PK_JACOBI>(zero, g, coef, hinv, f, u, w, s); return;
-    case HMG_VANKA_PLUS: go<T, R, PK_PLUS>(zero, g, coef, hinv, f, u, w, s); return;
+    case HMG_VANKA_RB: go<T, R, PK_RB>(zero, g, coef, hinv, f, u, uo, w, s); return;
+    case HMG_VANKA_ELEMENT: go<T, R, PK_ELEMENT>(zero, g, coef, hinv, f, u, uo, w, s); return;
+    case HMG_JACOBI: go<T, R, PK_JACOBI>(zero, g, coef, hinv, f, u, uo, w, s); return;
+    case HMG_VANKA_PLUS: go<T, R, PK_PLUS>(zero, g, coef, hinv, f, u, uo, w, s); return;
   }
   throw HmgError(HMG_EINVAL, "unknown smoother");
 }
 
 template <typename T>
 void smooth_stored2d(int r, int kind, bool zero, const Geo &g, const cplx<T> *coef, const cplx<T> *hinv,
-                     const double2 *f, double2 *u, double w, cudaStream_t s) {
+                     const double2 *f, const double2 *u, double2 *uo, double w, cudaStream_t s) {
   switch (r) {
-    case 1: go_kind<T, 1>(kind, zero, g, coef, hinv, f, u, w, s); return;
-    case 2: go_kind<T, 2>(kind, zero, g, coef, hinv, f, u, w, s); return;
-    case 3: go_kind<T, 3>(kind, zero, g, coef, hinv, f, u, w, s); return;
+    case 1: go_kind<T, 1>(kind, zero, g, coef, hinv, f, u, uo, w, s); return;
+    case 2: go_kind<T, 2>(kind, zero, g, coef, hinv, f, u, uo, w, s); return;
+    case 3: go_kind<T, 3>(kind, zero, g, coef, hinv, f, u, uo, w, s); return;
   }
   throw HmgError(HMG_EINVAL, "stencil radius out of range");
 }
 
 template void smooth_stored2d<float>(int, int, bool, const Geo &, const float2 *, const float2 *, const double2 *,
-                                     double2 *, double, cudaStream_t);
+                                     const double2 *, double2 *, double, cudaStream_t);
 template void smooth_stored2d<double>(int, int, bool, const Geo &, const double2 *, const double2 *, const double2 *,
-                                      double2 *, double, cudaStream_t);
+                                      const double2 *, double2 *, double, cudaStream_t);
 
 }  // namespace hmg

@@ -1,3 +1,6 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_multirank.py -q -p no:cacheprovider -x > gpurun_out/gpu_multirank.log 2>&1; echo exit=$? >> gpurun_out/gpu_multirank.log
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_exit=$? >> gpurun_out/bench.err
+CMD="python bench.py --n 2048 --steps 1 --warmup 1 --no-cpu-baseline"
+timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_rb2d_march" -s 0 -c 2 -o gpurun_out/prof_march $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu_full_exit=$? >> gpurun_out/ncu_full.log

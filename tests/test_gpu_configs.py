@@ -1,0 +1,78 @@
+"""End-to-end parity on the BASELINE.json configurations:
+FGMRES + V(1,1)-cycle through the C-ABI against the CPU oracle on the same
+seeded inputs.  Configs 1-4 run as scaled replicas (same generator, seed and
+physics) at sizes the oracle solves in seconds; config 0 is in
+test_gpu_parity.py.  Bar (north_star): iterations +-1 (c128) / +-2 (c64),
+true relative residual <= 1e-6 on both sides."""
+import numpy as np
+import pytest
+
+from helpers import DAMPING, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+def solve_both(p, levels, alpha, restart, dtype, smoother, maxiter=1000):
+    import torch
+    from paper_2511_16808_b200 import hmg
+    from oracle.cycle import vcycle
+    from oracle.fgmres import fgmres_solve
+    from oracle.hierarchy import Options as OOptions, build_hierarchy
+    damping = DAMPING[(p.dim, smoother)]
+    gh = hmg.Hierarchy(hmg.Options(dim=p.dim, cells=p.cells, h=p.h, levels=levels, smoother=smoother,
+                                   damping=damping, dtype=dtype), p.kappa, p.omega, p.gamma, alpha)
+    cdt = torch.complex64 if dtype == "c64" else torch.complex128
+    q = torch.from_numpy(p.q.ravel()).to(cdt).cuda()
+    x = torch.zeros_like(q)
+    rep = gh.fgmres_solve(q, x, restart=restart, tol=1e-6, maxiter=maxiter)
+    oh = build_hierarchy(OOptions(dim=p.dim, cells=p.cells, h=p.h, levels=levels, smoother=smoother,
+                                  damping=damping), p.kappa, p.omega, p.gamma, alpha)
+    xo, info = fgmres_solve(oh.H, p.q.ravel(), lambda v: vcycle(oh, v), restart=restart, tol=1e-6,
+                            maxiter=maxiter)
+    return rep, x.cpu().numpy().astype(np.complex128), info, xo
+
+
+def check(rep, x, info, xo, dtype):
+    assert rep.converged and rep.relres_true <= 1e-6
+    assert info["converged"]
+    slack = 1 if dtype == "c128" else 2
+    assert abs(rep.iterations - info["iterations"]) <= slack, (rep.iterations, info["iterations"])
+    assert rel_err(x, xo) <= (1e-4 if dtype == "c128" else 1e-3)
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_config1_n256(dtype):
+    """configs[1] family: 2D homogeneous, 16-node sponge, L = log2 N - 3, alpha 0.25, FGMRES(20)."""
+    from paper_2511_16808_b200 import media
+    p = media.config_problem(1, n=256)
+    check(*solve_both(p, 5, 0.25, 20, dtype, "rb"), dtype)
+
+
+def test_config2_quarter():
+    """configs[2] generator (seed 2, dipping layers + faults) at 1/4 resolution:
+    512 x 160 cells, h = 50 m, 8-node sponge, 5 levels, alpha 0.5, FGMRES(20)."""
+    from paper_2511_16808_b200 import media
+    p = media.config_problem(2, scale=4)
+    check(*solve_both(p, 5, 0.5, 20, "c128", "rb"), "c128")
+
+
+def test_config3_32cube():
+    """configs[3] family: 3D homogeneous, element patches, alpha 0.5, FGMRES(10), 32^3 cells, 3 levels."""
+    from paper_2511_16808_b200 import media
+    p = media.homogeneous_problem(3, 32, sponge=4, gamma_max_over_omega=2.0)
+    check(*solve_both(p, 3, 0.5, 10, "c64", "element"), "c64")
+
+
+def test_config4_replica():
+    """configs[4] generator (seed 4, folded layers + thrust fault) at 1/16 scale:
+    48 x 48 x 24 cells, h = 400 m, 3 levels, alpha 0.5, FGMRES(20), c64 fine / c128 coarsest."""
+    from paper_2511_16808_b200 import media
+    p = media.config_problem(4, scale=16)
+    check(*solve_both(p, 3, 0.5, 20, "c64", "element"), "c64")
