@@ -164,32 +164,40 @@ __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__
   const bool out_lane = lane >= 3 && lane < 3 + RB_STRIP && x < g.n[0];
   const D e = W::Le * ih2;
   const CD z = mkc<D>(0, 0);
-  auto in = [&](int y) { return g.inside(x, y, 0); };
-  // rolling window
-  CD um1 = z, u0 = z, up1 = z;          // u at rows b-1, b, b+1
-  CD ub1 = z;                           // u at row b-2 (the output row)
+  // x validity is fixed per lane; rows are checked against the global slab range
+  const bool xin = x + g.o[0] >= 0 && x + g.o[0] < g.N[0];
+  const int ylo = -g.o[1], yhi = g.N[1] - g.o[1];
+  auto in = [&](int y) { return xin && y >= ylo && y < yhi; };
+  // rolling window (u and ia stay in their storage type: converting on use is
+  // exact and keeps the register count down)
+  using CS = cplx<TS>;
+  const CS zs = mkc<TS>(0, 0);
+  CS um1 = zs, u0 = zs, up1 = zs;       // u at rows b-1, b, b+1
+  CS ub1 = zs;                          // u at row b-2 (the output row)
   CD r2 = z, r1 = z, r0 = z;            // r at rows b-2, b-1, b
   CD t2 = z, t1 = z, t0 = z;            // t = r ia at rows b-2, b-1, b
-  CD a2 = z, a1 = z, a0 = z;            // ia at rows b-2, b-1, b
+  CS a2 = zs, a1 = zs, a0 = zs;         // ia at rows b-2, b-1, b
   CD c3 = z, c2 = z, c1 = z;            // y_c at rows b-3, b-2, b-1
   // one-step-ahead prefetch registers, kept in the storage type so that the
   // loads of step b+1 stay in flight during step b
-  using CS = cplx<TS>;
-  const CS zs = mkc<TS>(0, 0);
-  auto lr = [&](const CS *a, int y) { return in(y) ? a[g.idx(x, y, 0)] : zs; };
+  // per-lane column offset; row y of array a sits at a + col + y * px
+  const int64_t col = g.base + x;
+  const int64_t px = g.px;
+  auto lr = [&](const CS *a, int y) { return in(y) ? a[col + (int64_t)y * px] : zs; };
   if (!ZERO) {
-    u0 = ccast<D, TS>(lr(u, y0 - 3));
-    up1 = ccast<D, TS>(lr(u, y0 - 2));
+    u0 = lr(u, y0 - 3);
+    up1 = lr(u, y0 - 2);
   }
   CS pu = ZERO ? zs : lr(u, y0 - 1), pf = lr(f, y0 - 2), pa = lr(ia_, y0 - 2), pid = lr(id_, y0 - 3);
   CS ps = ZERO ? zs : lr(sig, y0 - 2);
   for (int b = y0 - 2; b <= y1 + 1; ++b) {
     if (!ZERO) {
       ub1 = um1;
-      um1 = u0; u0 = up1; up1 = ccast<D, TS>(pu);
+      um1 = u0; u0 = up1; up1 = pu;
       pu = lr(u, b + 2);
     }
-    const CD fb = ccast<D, TS>(pf), ab = ccast<D, TS>(pa), idb = ccast<D, TS>(pid);
+    const CD fb = ccast<D, TS>(pf), idb = ccast<D, TS>(pid);
+    const CS ab = pa;
     CD sb = ccast<D, TS>(ps);
     pf = lr(f, b + 1);
     pa = lr(ia_, b + 1);
@@ -198,21 +206,25 @@ __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__
     // ---- r(b), t(b)  (fp64)
     CD rb = fb;
     if (!ZERO) {
-      const CD ul = shfl_up1(u0), ur = shfl_dn1(u0);
-      const CD uml = shfl_up1(um1), umr = shfl_dn1(um1), upl = shfl_up1(up1), upr = shfl_dn1(up1);
-      const CD sf = cadd<D>(cadd<D>(ul, ur), cadd<D>(um1, up1));
-      CD Lx = cscale<D>(u0, (D)W::Lc);
+      auto sh = [](CS v, bool up) {
+        return ccast<D, TS>(up ? mkc<TS>(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1))
+                               : mkc<TS>(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1)));
+      };
+      const CD uc = ccast<D, TS>(u0);
+      const CD sf = cadd<D>(cadd<D>(sh(u0, true), sh(u0, false)), cadd<D>(ccast<D, TS>(um1), ccast<D, TS>(up1)));
+      CD Lx = cscale<D>(uc, (D)W::Lc);
       Lx = cfmar<D>(Lx, (D)W::Lf, sf);
-      if (W::Le != 0.0) Lx = cfmar<D>(Lx, (D)W::Le, cadd<D>(cadd<D>(uml, umr), cadd<D>(upl, upr)));
+      if (W::Le != 0.0)
+        Lx = cfmar<D>(Lx, (D)W::Le, cadd<D>(cadd<D>(sh(um1, true), sh(um1, false)), cadd<D>(sh(up1, true), sh(up1, false))));
       Lx = cscale<D>(Lx, ih2);
-      CD Mx = cscale<D>(u0, (D)W::Mc);
+      CD Mx = cscale<D>(uc, (D)W::Mc);
       if (W::Mf != 0.0) Mx = cfmar<D>(Mx, (D)W::Mf, sf);
       sb.y = fma(-alpha, sb.x, sb.y);
       rb = in(b) ? csub<D>(fb, csub<D>(Lx, cmul<D>(sb, Mx))) : z;
     }
     r2 = r1; r1 = r0; r0 = rb;
     a2 = a1; a1 = a0; a0 = ab;
-    t2 = t1; t1 = t0; t0 = cmul<D>(rb, ab);
+    t2 = t1; t1 = t0; t0 = cmul<D>(rb, ccast<D, TS>(ab));
     // ---- y_c(b-1): diagonal leaves at rows b-2 and b, columns x +- 1
     {
       const CD sdiag = cadd<D>(cadd<D>(shfl_up1(t2), shfl_dn1(t2)), cadd<D>(shfl_up1(t0), shfl_dn1(t0)));
@@ -228,13 +240,15 @@ __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__
         // anchors j - (dx, dy) for the 4 diagonal offsets: rows yo -+ 1, columns x -+ 1
         CD syl = z;
         int k = 0;
-        if (g.inside(x - 1, yo - 1, 0)) { syl = cadd<D>(syl, cl3); ++k; }
-        if (g.inside(x + 1, yo - 1, 0)) { syl = cadd<D>(syl, cr3); ++k; }
-        if (g.inside(x - 1, yo + 1, 0)) { syl = cadd<D>(syl, cl1); ++k; }
-        if (g.inside(x + 1, yo + 1, 0)) { syl = cadd<D>(syl, cr1); ++k; }
-        const CD lv = cmul<D>(mkc<D>((D)k * r2.x - e * syl.x, (D)k * r2.y - e * syl.y), a2);
+        const bool xm = x - 1 + g.o[0] >= 0, xp = x + 1 + g.o[0] < g.N[0];
+        const bool ym = yo - 1 >= ylo, yp = yo + 1 < yhi;
+        if (xm && ym) { syl = cadd<D>(syl, cl3); ++k; }
+        if (xp && ym) { syl = cadd<D>(syl, cr3); ++k; }
+        if (xm && yp) { syl = cadd<D>(syl, cl1); ++k; }
+        if (xp && yp) { syl = cadd<D>(syl, cr1); ++k; }
+        const CD lv = cmul<D>(mkc<D>((D)k * r2.x - e * syl.x, (D)k * r2.y - e * syl.y), ccast<D, TS>(a2));
         const CD upd = cscale<D>(cadd<D>(c2, lv), w / (D)(1 + k));
-        u_out[g.idx(x, yo, 0)] = ccast<TS, D>(ZERO ? upd : cadd<D>(ub1, upd));
+        u_out[col + (int64_t)yo * px] = ccast<TS, D>(ZERO ? upd : cadd<D>(ccast<D, TS>(ub1), upd));
       }
     }
   }
