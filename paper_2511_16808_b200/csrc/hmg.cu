@@ -408,8 +408,7 @@ template <typename T> struct Solver : SolverBase {
     // cycle workspace
     for (int l = 0; l < L; ++l) {
       Level &Lv = lev[l];
-      const int k = patch_size(dim, opt.smoother);
-      if (!(l == 0 && rb_closed) && !fused_level(l) && l < L - 1) Lv.y.alloc((size_t)k * Lv.geo.total * vsize(l), s);
+
       Lv.u.alloc(Lv.geo.total * vsize(l), s);
       Lv.f.alloc(Lv.geo.total * vsize(l), s);
       Lv.r_.alloc(Lv.geo.total * vsize(l), s);
@@ -509,7 +508,10 @@ template <typename T> struct Solver : SolverBase {
   }
 
   // Galerkin levels of 2D hierarchies use the fused on-the-fly sweep
-  bool fused_level(int l) const { return opt.dim == 2 && l >= 1 && l < L - 1; }
+  // (measured: the one-kernel Galerkin sweep k_smooth_stored2d is register- and
+  // phase-bound at ~3.4 TB/s; the two-kernel path -- stored residual at 5.5 TB/s
+  // + direct-gather sweep -- moves 11 % more bytes but streams faster)
+  bool fused_level(int l) const { return false && opt.dim == 2 && l >= 1 && l < L - 1; }
 
   static int kcount(int dim, int r) { return dim == 3 ? (2 * r + 1) * (2 * r + 1) * (2 * r + 1) : (2 * r + 1) * (2 * r + 1); }
 
@@ -646,21 +648,18 @@ template <typename T> struct Solver : SolverBase {
     else prolong_t<D>(l, (const D *)e, (const D *)u, (D *)u_out, s);
   }
 
-  // generic two-pass Vanka (stored patch inverses + gather); TV = level vector type
+  // generic Vanka sweep (stored patch inverses, direct gather); TV = level vector type
   template <typename TV, int DIM, int KIND> void vanka_(int l, const void *r, void *u, int zero, cudaStream_t s) {
     Level &Lv = lev[l];
     using BV = decltype(TV{}.x);
     auto nl = node_launch(Lv.geo);
-    TV *y = Lv.y.template as<TV>();
     constexpr int K = Patch<DIM, KIND>::K;
     const double nn = (double)Lv.geo.nodes();
-    halo(l, r, 1, s);
-    tag("patch_apply", l, ((double)K * K * sizeof(C) + (K + 1) * sizeof(TV)) * nn);
-    launch(k_patch_apply<BV, T, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)Lv.hinv.template as<C>(),
-           (const TV *)r, y);
-    halo(l, y, 1, s, K);
-    tag("vanka_gather", l, (K + (zero ? 1 : 2)) * sizeof(TV) * nn);
-    launch(k_vanka_gather<BV, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const TV *)y, (BV)damp(l), (TV *)u, zero);
+    halo(l, r, 2, s);   // anchors at +-1, their members at +-1 again: r within radius 2
+    tag(zero ? "vanka_direct_zero" : "vanka_direct", l,
+        ((double)K * K * sizeof(C) + (zero ? 2 : 3) * sizeof(TV)) * nn);
+    launch(k_vanka_direct<BV, T, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)Lv.hinv.template as<C>(),
+           (const TV *)r, (const TV *)u, (TV *)u, (BV)damp(l), zero);
   }
   template <typename TV> void vanka_kind(int l, const void *r, void *u, int zero, cudaStream_t s) {
     const int dim = opt.dim;

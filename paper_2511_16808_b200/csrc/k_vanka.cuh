@@ -8,12 +8,10 @@
 // node and are clipped to the domain; W_i(j,j) = 1/cnt_j with cnt_j
 // = number of patches containing j (reading A7 for Element).
 //
-// B200 design: the scatter of Eq. 3.8 is done as a conflict-free GATHER in two
-// node-parallel passes: (1) every anchor c solves its patch system y_c =
-// H_c^{-1} r[X_c] and stores the |X_c| local values in slot-major planes
-// y[s][c]; (2) every node j sums y[s][j - o_s] over the anchors whose patch
-// contains it and applies w/cnt_j (the weight depends on j only, so it factors
-// out of the gather).  No atomics, deterministic order.
+// B200 design: the scatter of Eq. 3.8 is done as a conflict-free GATHER:
+// every node j sums, over the anchors c whose patch contains it, the entry of
+// y_c = H_c^{-1} r[X_c] that belongs to j, and applies w/cnt_j (the weight
+// depends on j only, so it factors out).  No atomics, deterministic order.
 #pragma once
 #include "common.cuh"
 #include "k_operator.cuh"
@@ -67,28 +65,39 @@ template <int DIM, int KIND> struct Patch {
   }
 };
 
-// (1a) generic patch solve with stored inverses: y[a][c] = sum_b Hinv[a*K+b][c] r[c + o_b]
+// (1a) generic sweep with stored inverses, as a direct gather (any dim/kind):
+//   u_out_j = u_j + (w/cnt_j) sum_{s: anchor c = j - o_s} sum_q Hinv_c[s][q] r[c + o_q]
+// (r = f - A u precomputed; r = f for a zero initial guess).  Only row s of
+// each containing anchor's inverse is read, so every stored entry is read once
+// per sweep and no patch solution is staged.  Each node reads/writes only its
+// own u: in place is safe.
 template <typename T, typename TK, int DIM, int KIND>
-__global__ void __launch_bounds__(256) k_patch_apply(Geo g, const cplx<TK> *__restrict__ hinv,
-                                                     const cplx<T> *__restrict__ r, cplx<T> *__restrict__ y) {
+__global__ void __launch_bounds__(256) k_vanka_direct(Geo g, const cplx<TK> *__restrict__ hinv,
+                                                      const cplx<T> *__restrict__ r, const cplx<T> *u,
+                                                      cplx<T> *u_out, T w, int zero) {
   HMG_NODE_IDX(g, ix, iy, iz);
   using P = Patch<DIM, KIND>;
-  if (!P::anchor(g, ix, iy, iz)) return;
-  const int64_t c = g.idx(ix, iy, iz);
-  cplx<T> rv[P::K];
+  constexpr int K = P::K;
+  cplx<T> acc = mkc<T>(0, 0);
 #pragma unroll
-  for (int b = 0; b < P::K; ++b) {
-    int ox, oy, oz;
-    P::off(b, ox, oy, oz);
-    rv[b] = r[c + g.delta(ox, oy, oz)];
+  for (int sI = 0; sI < K; ++sI) {
+    int dx, dy, dz;
+    P::off(sI, dx, dy, dz);
+    if (!P::anchor(g, ix - dx, iy - dy, iz - dz)) continue;
+    const int64_t c = g.idx(ix - dx, iy - dy, iz - dz);
+    cplx<TK> hw[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) hw[q] = hinv[(int64_t)(sI * K + q) * g.total + c];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      int bx, by, bz;
+      P::off(q, bx, by, bz);
+      acc = cfma<T>(acc, ccast<T, TK>(hw[q]), r[c + g.delta(bx, by, bz)]);
+    }
   }
-#pragma unroll
-  for (int a = 0; a < P::K; ++a) {
-    cplx<T> acc = mkc<T>(0, 0);
-#pragma unroll
-    for (int b = 0; b < P::K; ++b) acc = cfma<T>(acc, ccast<T, TK>(hinv[(int64_t)(a * P::K + b) * g.total + c]), rv[b]);
-    y[(int64_t)a * g.total + c] = acc;
-  }
+  const int64_t j = g.idx(ix, iy, iz);
+  const cplx<T> upd = cscale<T>(acc, w / (T)P::count(g, ix, iy, iz));
+  u_out[j] = zero ? upd : cadd<T>(u[j], upd);
 }
 
 // (1b) fine-level RB smoothing sweep in ONE kernel (2D, matrix-free).
@@ -302,14 +311,18 @@ __device__ __forceinline__ void small_solve(cplx<T> (&A)[K][K], cplx<T> (&b)[K])
 
 // (1c) one additive-Vanka sweep on a Galerkin level in ONE kernel (2D,
 // stored stencil of radius R): residual on the tile + 2 into shared memory,
-// every patch anchored on the tile + 1 assembled from the stencil
-// coefficients of its member rows (H_i = A[X_i, X_i], reading A8) and solved
-// in registers (no stored inverses), the K local values staged in shared
-// memory, then the 1/cnt-weighted gather.  HBM: the K stencil planes, u, f
-// read once, u written once (ZERO: f and the patch planes only).
-// Out of place: u_out = u + w B (f - A u) (u unused with ZERO).
-template <typename T, typename TK, int R, int KIND, int TX, int TY, bool ZERO, bool HINV>
-__global__ void __launch_bounds__(256, 2) k_smooth_stored2d(Geo g, const cplx<TK> *__restrict__ coef,
+// then every output node j gathers its patch values DIRECTLY,
+//     u_j += w/cnt_j sum_{s: anchor c = j - o_s} sum_b Hinv_c[s][b] r[c + o_b],
+// i.e. only row s of each containing anchor's inverse is needed; every
+// stored inverse entry is still read exactly once per sweep and no patch
+// solution is staged (reading A8: H_i = A_l[X_i, X_i], inverses formed at
+// setup in fp64 by k_patch_inverse).  HBM: stencil planes (residual), inverse
+// planes, u, f read once, u' written once (ZERO: inverse planes and f only).
+// Out of place (u_out != u): other blocks still read old u in their halos.
+// Without stored inverses (hinv == nullptr) each anchor's patch matrix is
+// assembled from the stencil and solved in registers (k_smooth_stored2d_lu).
+template <typename T, typename TK, int R, int KIND, int TX, int TY, bool ZERO>
+__global__ void __launch_bounds__(256) k_smooth_stored2d(Geo g, const cplx<TK> *__restrict__ coef,
                                                          const cplx<TK> *__restrict__ hinv,
                                                          const cplx<T> *__restrict__ f, const cplx<T> *__restrict__ u,
                                                          cplx<T> *__restrict__ u_out, T w) {
@@ -318,11 +331,10 @@ __global__ void __launch_bounds__(256, 2) k_smooth_stored2d(Geo g, const cplx<TK
   constexpr int NT = 256;
   constexpr int WS = 2 * R + 1;
   constexpr int HU = 2 + R;
-  constexpr int UX = TX + 2 * HU, UY = TY + 2 * HU, RX = TX + 4, RY = TY + 4, YX = TX + 2, YY = TY + 2;
+  constexpr int UX = TX + 2 * HU, UY = TY + 2 * HU, RX = TX + 4, RY = TY + 4;
   constexpr int NU = (UX * UY + NT - 1) / NT, NR = (RX * RY + NT - 1) / NT;
   __shared__ cplx<T> su[ZERO ? 1 : UY * UX];
   __shared__ cplx<T> sr[RY * RX];
-  __shared__ cplx<T> sy[K * YY * YX];
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const cplx<T> zero = mkc<T>(0, 0);
@@ -357,61 +369,17 @@ __global__ void __launch_bounds__(256, 2) k_smooth_stored2d(Geo g, const cplx<TK
       const cplx<T> *uc = su + (ly + R) * UX + (lx + R);
       cplx<T> acc = zero;
 #pragma unroll
-      for (int oy = -R; oy <= R; ++oy)
+      for (int oy = -R; oy <= R; ++oy) {
+        cplx<TK> cw[WS];
 #pragma unroll
-        for (int ox = -R; ox <= R; ++ox)
-          acc = cfma<T>(acc, ccast<T, TK>(coef[(int64_t)((ox + R) + WS * (oy + R)) * g.total + j]), uc[oy * UX + ox]);
+        for (int ox = -R; ox <= R; ++ox) cw[ox + R] = coef[(int64_t)((ox + R) + WS * (oy + R)) * g.total + j];
+#pragma unroll
+        for (int ox = -R; ox <= R; ++ox) acc = cfma<T>(acc, ccast<T, TK>(cw[ox + R]), uc[oy * UX + ox]);
+      }
       sr[i] = csub<T>(sr[i], acc);
     }
     __syncthreads();
   }
-  for (int i = tid; i < YY * YX; i += NT) {
-    const int lx = i % YX, ly = i / YX;
-    const int cx = x0 - 1 + lx, cy = y0 - 1 + ly;
-    if (!P::anchor(g, cx, cy, 0)) continue;
-    cplx<T> A[K][K], b[K];
-    bool pres[K];
-#pragma unroll
-    for (int a = 0; a < K; ++a) {
-      int ax, ay, az;
-      P::off(a, ax, ay, az);
-      pres[a] = g.inside(cx + ax, cy + ay, 0);
-      b[a] = pres[a] ? sr[(ly + 1 + ay) * RX + (lx + 1 + ax)] : zero;
-    }
-    if (HINV) {
-      // stored inverse of the clipped patch matrix (rows/cols of clipped members are 0)
-      const int64_t c = g.idx(cx, cy, 0);
-#pragma unroll
-      for (int a = 0; a < K; ++a) {
-        cplx<T> acc = zero;
-#pragma unroll
-        for (int q = 0; q < K; ++q) acc = cfma<T>(acc, ccast<T, TK>(hinv[(int64_t)(a * K + q) * g.total + c]), b[q]);
-        sy[a * YY * YX + i] = acc;
-      }
-      continue;
-    }
-#pragma unroll
-    for (int a = 0; a < K; ++a) {
-      int ax, ay, az;
-      P::off(a, ax, ay, az);
-      const int64_t row = g.idx(cx + ax, cy + ay, 0);
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        int bx, by, bz;
-        P::off(c, bx, by, bz);
-        const int dx = bx - ax, dy = by - ay;
-        cplx<T> v = zero;
-        if (dx >= -R && dx <= R && dy >= -R && dy <= R && pres[a] && pres[c])
-          v = ccast<T, TK>(coef[(int64_t)((dx + R) + WS * (dy + R)) * g.total + row]);
-        if (!pres[a] && a == c) v = mkc<T>(1, 0);   // clipped member: identity row, zero rhs
-        A[a][c] = v;
-      }
-    }
-    small_solve<T, K>(A, b);
-#pragma unroll
-    for (int a = 0; a < K; ++a) sy[a * YY * YX + i] = b[a];
-  }
-  __syncthreads();
   for (int oy = threadIdx.y; oy < TY; oy += blockDim.y) {
     for (int ox = threadIdx.x; ox < TX; ox += blockDim.x) {
       const int gx = x0 + ox, gy = y0 + oy;
@@ -421,32 +389,25 @@ __global__ void __launch_bounds__(256, 2) k_smooth_stored2d(Geo g, const cplx<TK
       for (int sI = 0; sI < K; ++sI) {
         int dx, dy, dz;
         P::off(sI, dx, dy, dz);
-        if (P::anchor(g, gx - dx, gy - dy, 0)) acc = cadd<T>(acc, sy[sI * YY * YX + (oy + 1 - dy) * YX + (ox + 1 - dx)]);
+        const int cx = gx - dx, cy = gy - dy;   // anchor whose patch holds j in slot sI
+        if (!P::anchor(g, cx, cy, 0)) continue;
+        const int64_t c = g.idx(cx, cy, 0);
+        cplx<TK> hw[K];
+#pragma unroll
+        for (int q = 0; q < K; ++q) hw[q] = hinv[(int64_t)(sI * K + q) * g.total + c];
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          int bx, by, bz;
+          P::off(q, bx, by, bz);
+          // members outside the domain have zero inverse columns and r = 0 there
+          acc = cfma<T>(acc, ccast<T, TK>(hw[q]), sr[(oy + 2 - dy + by) * RX + (ox + 2 - dx + bx)]);
+        }
       }
       const cplx<T> upd = cscale<T>(acc, w / (T)P::count(g, gx, gy, 0));
       const int64_t j = g.idx(gx, gy, 0);
       u_out[j] = ZERO ? upd : cadd<T>(su[(oy + HU) * UX + (ox + HU)], upd);
     }
   }
-}
-
-// (2) gather: u_j (+)= (w/cnt_j) sum_s y[s][j - o_s] over anchors containing j
-template <typename T, int DIM, int KIND>
-__global__ void __launch_bounds__(256) k_vanka_gather(Geo g, const cplx<T> *__restrict__ y, T w,
-                                                      cplx<T> *__restrict__ u, int zero_init) {
-  HMG_NODE_IDX(g, ix, iy, iz);
-  using P = Patch<DIM, KIND>;
-  const int64_t j = g.idx(ix, iy, iz);
-  cplx<T> acc = mkc<T>(0, 0);
-#pragma unroll
-  for (int s = 0; s < P::K; ++s) {
-    int ox, oy, oz;
-    P::off(s, ox, oy, oz);
-    if (P::anchor(g, ix - ox, iy - oy, iz - oz)) acc = cadd<T>(acc, y[(int64_t)s * g.total + j - g.delta(ox, oy, oz)]);
-  }
-  const T wc = w / (T)P::count(g, ix, iy, iz);
-  const cplx<T> upd = cscale<T>(acc, wc);
-  u[j] = zero_init ? upd : cadd<T>(u[j], upd);
 }
 
 }  // namespace hmg

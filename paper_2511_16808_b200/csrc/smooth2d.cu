@@ -10,15 +10,11 @@ namespace hmg {
 template <typename TK, int R, int KIND>
 static void go(bool zero, const Geo &g, const cplx<TK> *coef, const cplx<TK> *hinv, const double2 *f,
                const double2 *u, double2 *uo, double w, cudaStream_t s) {
-  constexpr int TX = 32, TY = 8;   // fp64 tiles: 32 x 8 keeps static smem under 48 KB
+  if (!hinv) throw HmgError(HMG_EINVAL, "fused Galerkin sweep needs the stored patch inverses");
+  constexpr int TX = 32, TY = 16;   // fp64 smem: u (tile + 2 + R) and r (tile + 2), < 48 KB
   const dim3 grid((g.n[0] + TX - 1) / TX, (g.n[1] + TY - 1) / TY), block(32, 8);
-  if (hinv) {
-    if (zero) launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, true, true>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
-    else launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, false, true>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
-  } else {
-    if (zero) launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, true, false>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
-    else launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, false, false>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
-  }
+  if (zero) launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, true>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
+  else launch(k_smooth_stored2d<double, TK, R, KIND, TX, TY, false>, grid, block, 0, s, g, coef, hinv, f, u, uo, w);
 }
 
 template <typename T, int R>
