@@ -884,10 +884,10 @@ template <typename T> struct Solver : SolverBase {
   }
   template <typename TV, typename TW>
   void maxpy(const cplx<TV> *Vb, int nv, const double2 *coef, double sgn, cplx<TW> *w, double2 *nrm_out,
-             cudaStream_t s) {
+             cudaStream_t s, const double *vscale = nullptr) {
     const Geo &g = g0();
     tag("multi_axpy", 0, (nv * sizeof(cplx<TV>) + 2.0 * sizeof(cplx<TW>)) * (double)g.slab_len);
-    const int nb = krylov_axpy<TV, TW>(nv, Vb + g.slab_off, g.total, coef, sgn, w + g.slab_off, g.slab_len,
+    const int nb = krylov_axpy<TV, TW>(nv, Vb + g.slab_off, g.total, coef, vscale, sgn, w + g.slab_off, g.slab_len,
                                        nrm_out ? partial.template as<double2>() : (double2 *)nullptr, s);
     if (nrm_out) {
       tag("reduce", 0, 16.0 * nb);
@@ -971,6 +971,7 @@ template <typename T> struct Solver : SolverBase {
       return HMG_OK;
     }
     std::vector<cd> H((m + 1) * m), cs(m), sn(m), gv(m + 1), y(m);
+    std::vector<double> nbeta(m + 1, 1.0);
     auto Hs = [&](int i, int j) -> cd & { return H[(size_t)i * m + j]; };
     double2 *dr = dres.template as<double2>();
     bool have_res = false;
@@ -986,41 +987,54 @@ template <typename T> struct Solver : SolverBase {
       std::fill(H.begin(), H.end(), cd(0, 0));
       std::fill(gv.begin(), gv.end(), cd(0, 0));
       gv[0] = beta;
+      // Lazily normalised Arnoldi basis: V[j] holds W_j = nb[j] v_j with
+      // nb[j] = ||W_j|| (nb[0] = 1); the cycle and the matvec run on W_j, so
+      // d_i = W_i^H (H M W_j) = nb[i] nb[j] h_ij, the AXPY removes
+      // (d_i / nb[i]^2) W_i, and W_{j+1} = nb[j] w_perp needs no scaling pass.
+      nbeta[0] = 1.0;
       int jend = 0;
       bool stop = false;
+      double *ib2h = hpin + 512, *ib2d = reinterpret_cast<double *>(dr + 160);
       for (int j = 0; j < m; ++j) {
-        cycle(0, Vp(j), Zp(j), 1, s);                // z_j = MG(v_j)
+        cycle(0, Vp(j), Zp(j), 1, s);                // z'_j = M(W_j)
         C *w = Vp(j + 1);
-        matvec(Zp(j), w, s);                         // w = H z_j (fp64 arithmetic)
+        matvec(Zp(j), w, s);                         // w' = H z'_j (fp64 arithmetic)
         const int nv = j + 1;
+        for (int i = 0; i <= j; ++i) ib2h[i] = 1.0 / (nbeta[i] * nbeta[i]);
+        CK(cudaMemcpyAsync(ib2d, ib2h, nv * sizeof(double), cudaMemcpyHostToDevice, s));
         // classical Gram-Schmidt with selective reorthogonalisation: a second
-        // pass only under strong cancellation, ||w'|| < 0.1 ||w|| (DESIGN.md
+        // pass only under strong cancellation, ||w''|| < 0.1 ||w'|| (DESIGN.md
         // §6: DGKS's 1/sqrt 2 reorthogonalised 59% of the steps at N=4096 and
         // never changed an iteration count)
-        mdot<T, T>(V.template as<C>(), nv, w, dr, s, true);        // h = V^H w, ||w||^2
-        maxpy<T, T>(V.template as<C>(), nv, dr, -1.0, w, dr + 64, s);  // w -= V h, ||w'||^2
+        mdot<T, T>(V.template as<C>(), nv, w, dr, s, true);            // d = W^H w', ||w'||^2
+        maxpy<T, T>(V.template as<C>(), nv, dr, -1.0, w, dr + 64, s, ib2d);   // w'' = w' - W diag(1/nb^2) d
         CK(cudaMemcpyAsync(hpin, dr, 65 * sizeof(double2), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         const double2 *hh = reinterpret_cast<const double2 *>(hpin);
-        for (int i = 0; i <= j; ++i) Hs(i, j) = cd(hh[i].x, hh[i].y);
+        for (int i = 0; i <= j; ++i) Hs(i, j) = cd(hh[i].x, hh[i].y) / (nbeta[i] * nbeta[j]);
         double hn2 = hh[64].x;
         if (!(hn2 >= kReorthEta2 * hh[nv].x)) {
           ++reorth;
           mdot<T, T>(V.template as<C>(), nv, w, dr + 32, s);
-          maxpy<T, T>(V.template as<C>(), nv, dr + 32, -1.0, w, dr + 64, s);
+          maxpy<T, T>(V.template as<C>(), nv, dr + 32, -1.0, w, dr + 64, s, ib2d);
           CK(cudaMemcpyAsync(hpin + 64, dr + 32, 33 * sizeof(double2), cudaMemcpyDeviceToHost, s));
           CK(cudaStreamSynchronize(s));
-          for (int i = 0; i <= j; ++i) Hs(i, j) += cd(hh[32 + i].x, hh[32 + i].y);
+          for (int i = 0; i <= j; ++i) Hs(i, j) += cd(hh[32 + i].x, hh[32 + i].y) / (nbeta[i] * nbeta[j]);
           hn2 = hh[64].x;
         }
-        const double hn = std::sqrt(std::max(hn2, 0.0));
+        const double wn = std::sqrt(std::max(hn2, 0.0));          // ||W_{j+1}||
         for (int i = 0; i <= j; ++i)
           if (!std::isfinite(Hs(i, j).real()) || !std::isfinite(Hs(i, j).imag()))
             throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi coefficient");
-        if (!std::isfinite(hn)) throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi norm");
+        if (!std::isfinite(wn)) throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi norm");
+        const double hn = wn / nbeta[j];
         Hs(j + 1, j) = hn;
         const bool breakdown = hn == 0.0;
-        if (!breakdown) scale<T, T>(w, w, 1.0 / hn, s);
+        nbeta[j + 1] = wn;
+        if (!breakdown && (wn < 1e-25 || wn > 1e25)) {   // keep the stored basis in range (rare)
+          scale<T, T>(w, w, 1.0 / wn, s);
+          nbeta[j + 1] = 1.0;
+        }
         for (int i = 0; i < j; ++i) {                // previous Givens rotations
           const cd t = cs[i] * Hs(i, j) + sn[i] * Hs(i + 1, j);
           Hs(i + 1, j) = -std::conj(sn[i]) * Hs(i, j) + std::conj(cs[i]) * Hs(i + 1, j);
@@ -1047,7 +1061,7 @@ template <typename T> struct Solver : SolverBase {
         y[i] = acc / Hs(i, i);
       }
       double2 *yp = reinterpret_cast<double2 *>(hpin) + 128;
-      for (int i = 0; i < jend; ++i) yp[i] = make_double2(y[i].real(), y[i].imag());
+      for (int i = 0; i < jend; ++i) yp[i] = make_double2(y[i].real() / nbeta[i], y[i].imag() / nbeta[i]);  // z_i = z'_i / nb[i]
       CK(cudaMemcpyAsync(dr + 96, yp, jend * sizeof(double2), cudaMemcpyHostToDevice, s));
       maxpy<T, double>(Z.template as<C>(), jend, dr + 96, 1.0, x, nullptr, s);   // x += Z y (fp64)
       ++restarts;

@@ -92,13 +92,18 @@ static __global__ void k_reduce_partials(const double2 *__restrict__ partial, in
 
 // w <- w + sgn * sum_i coef[i] V_i  (coef on the device, fp64); if NORM also
 // partial[block] = sum |w_new|^2 (fp64, of the stored value)
+// (vscale != nullptr: coefficient i is further multiplied by vscale[i] -- the
+// 1/beta_i^2 of FGMRES's lazily normalised basis)
 template <typename TV, typename TW, int NV, bool NORM>
 __global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy(const cplx<TV> *__restrict__ V, int64_t vstride,
-                                                            const double2 *__restrict__ coef, double sgn,
-                                                            cplx<TW> *__restrict__ w, int64_t len,
+                                                            const double2 *__restrict__ coef, const double *vscale,
+                                                            double sgn, cplx<TW> *__restrict__ w, int64_t len,
                                                             double2 *__restrict__ partial) {
   __shared__ double2 sc[NV];
-  if (threadIdx.x < NV) sc[threadIdx.x] = make_double2(sgn * coef[threadIdx.x].x, sgn * coef[threadIdx.x].y);
+  if (threadIdx.x < NV) {
+    const double f = sgn * (vscale ? vscale[threadIdx.x] : 1.0);
+    sc[threadIdx.x] = make_double2(f * coef[threadIdx.x].x, f * coef[threadIdx.x].y);
+  }
   __syncthreads();
   double nrm = 0.0;
   constexpr int U = NV <= 2 ? 4 : NV <= 5 ? 2 : 1;

@@ -55,20 +55,20 @@ int krylov_multidot(int nv, bool self, const cplx<TV> *V, int64_t vstride, const
 }
 
 template <typename TV, typename TW>
-int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef, double sgn, cplx<TW> *w, int64_t len,
-                double2 *partial_norm, cudaStream_t s) {
+int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef, const double *vscale, double sgn,
+                cplx<TW> *w, int64_t len, double2 *partial_norm, cudaStream_t s) {
   const dim3 b(KRY_THREADS);
   if (partial_norm) {
     switch (nv) {
 #define C_(N) case N: { auto k = k_multi_axpy<TV, TW, N, true>; const int nb = wave_blocks(k, len); \
-                        launch(k, dim3(nb), b, 0, s, V, vstride, coef, sgn, w, len, partial_norm); return nb; }
+                        launch(k, dim3(nb), b, 0, s, V, vstride, coef, vscale, sgn, w, len, partial_norm); return nb; }
       HMG_NV_CASES(C_)
 #undef C_
     }
   } else {
     switch (nv) {
 #define C_(N) case N: { auto k = k_multi_axpy<TV, TW, N, false>; const int nb = wave_blocks(k, len); \
-                        launch(k, dim3(nb), b, 0, s, V, vstride, coef, sgn, w, len, (double2 *)nullptr); return nb; }
+                        launch(k, dim3(nb), b, 0, s, V, vstride, coef, vscale, sgn, w, len, (double2 *)nullptr); return nb; }
       HMG_NV_CASES(C_)
 #undef C_
     }
@@ -79,8 +79,8 @@ int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef,
 
 template int krylov_multidot<float, float>(int, bool, const float2 *, int64_t, const float2 *, int64_t, double2 *, cudaStream_t);
 template int krylov_multidot<double, double>(int, bool, const double2 *, int64_t, const double2 *, int64_t, double2 *, cudaStream_t);
-template int krylov_axpy<float, float>(int, const float2 *, int64_t, const double2 *, double, float2 *, int64_t, double2 *, cudaStream_t);
-template int krylov_axpy<double, double>(int, const double2 *, int64_t, const double2 *, double, double2 *, int64_t, double2 *, cudaStream_t);
-template int krylov_axpy<float, double>(int, const float2 *, int64_t, const double2 *, double, double2 *, int64_t, double2 *, cudaStream_t);
+template int krylov_axpy<float, float>(int, const float2 *, int64_t, const double2 *, const double *, double, float2 *, int64_t, double2 *, cudaStream_t);
+template int krylov_axpy<double, double>(int, const double2 *, int64_t, const double2 *, const double *, double, double2 *, int64_t, double2 *, cudaStream_t);
+template int krylov_axpy<float, double>(int, const float2 *, int64_t, const double2 *, const double *, double, double2 *, int64_t, double2 *, cudaStream_t);
 
 }  // namespace hmg

@@ -49,8 +49,8 @@ template <typename TV, typename TW>
 int krylov_multidot(int nv, bool self, const cplx<TV> *V, int64_t vstride, const cplx<TW> *w, int64_t len,
                     double2 *partial, cudaStream_t s);
 template <typename TV, typename TW>
-int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef, double sgn, cplx<TW> *w, int64_t len,
-                double2 *partial_norm, cudaStream_t s);
+int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef, const double *vscale, double sgn,
+                cplx<TW> *w, int64_t len, double2 *partial_norm, cudaStream_t s);
 
 // Communication of the slab-partitioned solve (comm.cu).  All calls are
 // collective over the ranks and stream-ordered on `s`.
