@@ -631,15 +631,22 @@ template <typename T> struct Solver : SolverBase {
   template <typename TU> void prolong_t(int l, const D *e, const TU *u, TU *uo, cudaStream_t s) {
     const Level &F = lev[l], &Cc = lev[l + 1];
     halo(l + 1, e, 1, s);
-    auto nl = node_launch(F.geo);
     using BU = decltype(u->x);
     tag("prolong_add", l, 2.0 * sizeof(TU) * F.geo.nodes() + (double)sizeof(D) * Cc.geo.nodes());
+    // coarse nodes (global) whose 2x..2x+1 fine children touch this rank's fine rows
+    int c0[3], nc[3];
+    for (int a = 0; a < 3; ++a) {
+      const int flo = F.geo.o[a], fhi = F.geo.o[a] + F.geo.n[a];   // global fine range
+      c0[a] = flo / 2;
+      nc[a] = (fhi - 1) / 2 - c0[a] + 1;
+    }
+    const dim3 block(32, 8), grid((nc[0] + 31) / 32, (nc[1] + 7) / 8, opt.dim == 3 ? nc[2] : 1);
     if (opt.dim == 2) {
-      if (F.rP == 1) launch(k_prolong_add<double, BU, 2, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u, uo);
-      else launch(k_prolong_add<double, BU, 2, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u, uo);
+      if (F.rP == 1) launch(k_prolong_block<double, BU, 2, 1>, grid, block, 0, s, F.geo, Cc.geo, c0[0], c0[1], c0[2], nc[0], nc[1], nc[2], e, u, uo);
+      else launch(k_prolong_block<double, BU, 2, 2>, grid, block, 0, s, F.geo, Cc.geo, c0[0], c0[1], c0[2], nc[0], nc[1], nc[2], e, u, uo);
     } else {
-      if (F.rP == 1) launch(k_prolong_add<double, BU, 3, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u, uo);
-      else launch(k_prolong_add<double, BU, 3, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, e, u, uo);
+      if (F.rP == 1) launch(k_prolong_block<double, BU, 3, 1>, grid, block, 0, s, F.geo, Cc.geo, c0[0], c0[1], c0[2], nc[0], nc[1], nc[2], e, u, uo);
+      else launch(k_prolong_block<double, BU, 3, 2>, grid, block, 0, s, F.geo, Cc.geo, c0[0], c0[1], c0[2], nc[0], nc[1], nc[2], e, u, uo);
     }
   }
   // u_out = u + P_l e  (u_out may be u)

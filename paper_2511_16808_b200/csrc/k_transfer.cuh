@@ -104,4 +104,63 @@ __global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<
   u_out[i] = ccast<TU, T>(cadd<T>(ccast<T, TU>(u[i]), acc));
 }
 
+// Same operation, coarse-node parallel: the thread of coarse node J writes
+// the 2^d fine nodes 2J + {0,1}^d (global parity), loading its 3^d coarse
+// neighbourhood once (instead of up to 3^d loads per fine node).  Fine nodes
+// outside this rank's rows / the domain are skipped.  u_out may equal u.
+template <typename TE, typename TU, int DIM, int PR>
+__global__ void __launch_bounds__(256) k_prolong_block(Geo gf, Geo gc, int cx0, int cy0, int cz0, int ncx, int ncy,
+                                                       int ncz, const cplx<TE> *__restrict__ e, const cplx<TU> *u,
+                                                       cplx<TU> *u_out) {
+  using T = double;
+  const int X = cx0 + (int)(blockIdx.x * blockDim.x + threadIdx.x);   // GLOBAL coarse coordinates
+  const int Y = cy0 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+  const int Z = cz0 + (int)blockIdx.z;
+  if (X >= cx0 + ncx || Y >= cy0 + ncy || (DIM == 3 && Z >= cz0 + ncz)) return;
+  constexpr int ZW = DIM == 3 ? 3 : 1;
+  cplx<T> c[ZW][3][3];
+#pragma unroll
+  for (int dz = 0; dz < ZW; ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const int jx = X - 1 + dx - gc.o[0], jy = Y - 1 + dy - gc.o[1], jz = DIM == 3 ? Z - 1 + dz - gc.o[2] : 0;
+        c[dz][dy][dx] = ccast<T, TE>(e[gc.idx(jx, jy, jz)]);   // coarse ghosts are zero / halo
+      }
+  // 1D weights of fine parity p (0 even, 1 odd) on coarse offsets -1, 0, +1
+  auto wt = [](int p, int k) -> double {
+    if (p == 0) return PR == 2 ? (k == 1 ? 0.75 : 0.125) : (k == 1 ? 1.0 : 0.0);
+    return k == 0 ? 0.0 : 0.5;   // odd fine 2J+1: J (k=1) and J+1 (k=2)
+  };
+#pragma unroll
+  for (int pz = 0; pz < (DIM == 3 ? 2 : 1); ++pz)
+#pragma unroll
+    for (int py = 0; py < 2; ++py)
+#pragma unroll
+      for (int px = 0; px < 2; ++px) {
+        const int fx = 2 * X + px - gf.o[0], fy = 2 * Y + py - gf.o[1], fz = DIM == 3 ? 2 * Z + pz - gf.o[2] : 0;
+        if (fx < 0 || fx >= gf.n[0] || fy < 0 || fy >= gf.n[1] || (DIM == 3 && (fz < 0 || fz >= gf.n[2]))) continue;
+        cplx<T> acc = mkc<T>(0, 0);
+#pragma unroll
+        for (int dz = 0; dz < ZW; ++dz) {
+          const double wz = DIM == 3 ? wt(pz, dz) : 1.0;
+          if (wz == 0.0) continue;
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy) {
+            const double wy = wt(py, dy);
+            if (wy == 0.0) continue;
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+              const double wx = wt(px, dx);
+              if (wx == 0.0) continue;
+              acc = cfmar<T>(acc, wx * wy * wz, c[dz][dy][dx]);
+            }
+          }
+        }
+        const int64_t i = gf.idx(fx, fy, fz);
+        u_out[i] = ccast<TU, T>(cadd<T>(ccast<T, TU>(u[i]), acc));
+      }
+}
+
 }  // namespace hmg
