@@ -148,19 +148,28 @@ __device__ __forceinline__ double2 shfl_up1(double2 v) {
 __device__ __forceinline__ double2 shfl_dn1(double2 v) {
   return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
 }
+__device__ __forceinline__ float2 shfl_up1(float2 v) {
+  return make_float2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ float2 shfl_dn1(float2 v) {
+  return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
 
 constexpr int RB_STRIP = 26;
 
 // Out of place: u_out = u_in + w B (f - H_s u_in) (u_in unused with ZERO).  In
 // place would race: other warps still read old u in their halo rows/columns.
-template <typename TS, int KIND, bool ZERO, int SEG>
+// TC = arithmetic precision of the patch algebra (fp64, or the storage
+// precision), TR = precision of the residual f - H_s u
+template <typename TS, int KIND, bool ZERO, int SEG, typename TC = double, typename TR = double>
 __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__restrict__ sig,
                                                     const cplx<TS> *__restrict__ ia_, const cplx<TS> *__restrict__ id_,
-                                                    double alpha, double ih2, const cplx<TS> *__restrict__ f,
+                                                    double alpha_d, double ih2_d, const cplx<TS> *__restrict__ f,
                                                     const cplx<TS> *__restrict__ u, cplx<TS> *__restrict__ u_out,
-                                                    double w) {
+                                                    double w_d) {
   using W = FineW<2, KIND>;
-  using D = double;
+  using D = TC;
+  const D alpha = (D)alpha_d, ih2 = (D)ih2_d, w = (D)w_d;
   using CD = cplx<D>;
   const int lane = threadIdx.x & 31;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -205,31 +214,34 @@ __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__
       um1 = u0; u0 = up1; up1 = pu;
       pu = lr(u, b + 2);
     }
+    const CS pf_cur = pf, ps_cur = ps;
     const CD fb = ccast<D, TS>(pf), idb = ccast<D, TS>(pid);
     const CS ab = pa;
-    CD sb = ccast<D, TS>(ps);
     pf = lr(f, b + 1);
     pa = lr(ia_, b + 1);
     pid = lr(id_, b);
     if (!ZERO) ps = lr(sig, b + 1);
-    // ---- r(b), t(b)  (fp64)
+    // ---- r(b) in TR, t(b)
     CD rb = fb;
     if (!ZERO) {
+      using Q = TR;
+      using CQ = cplx<Q>;
       auto sh = [](CS v, bool up) {
-        return ccast<D, TS>(up ? mkc<TS>(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1))
+        return ccast<Q, TS>(up ? mkc<TS>(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1))
                                : mkc<TS>(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1)));
       };
-      const CD uc = ccast<D, TS>(u0);
-      const CD sf = cadd<D>(cadd<D>(sh(u0, true), sh(u0, false)), cadd<D>(ccast<D, TS>(um1), ccast<D, TS>(up1)));
-      CD Lx = cscale<D>(uc, (D)W::Lc);
-      Lx = cfmar<D>(Lx, (D)W::Lf, sf);
+      const CQ uc = ccast<Q, TS>(u0);
+      const CQ sf = cadd<Q>(cadd<Q>(sh(u0, true), sh(u0, false)), cadd<Q>(ccast<Q, TS>(um1), ccast<Q, TS>(up1)));
+      CQ Lx = cscale<Q>(uc, (Q)W::Lc);
+      Lx = cfmar<Q>(Lx, (Q)W::Lf, sf);
       if (W::Le != 0.0)
-        Lx = cfmar<D>(Lx, (D)W::Le, cadd<D>(cadd<D>(sh(um1, true), sh(um1, false)), cadd<D>(sh(up1, true), sh(up1, false))));
-      Lx = cscale<D>(Lx, ih2);
-      CD Mx = cscale<D>(uc, (D)W::Mc);
-      if (W::Mf != 0.0) Mx = cfmar<D>(Mx, (D)W::Mf, sf);
-      sb.y = fma(-alpha, sb.x, sb.y);
-      rb = in(b) ? csub<D>(fb, csub<D>(Lx, cmul<D>(sb, Mx))) : z;
+        Lx = cfmar<Q>(Lx, (Q)W::Le, cadd<Q>(cadd<Q>(sh(um1, true), sh(um1, false)), cadd<Q>(sh(up1, true), sh(up1, false))));
+      Lx = cscale<Q>(Lx, (Q)ih2_d);
+      CQ Mx = cscale<Q>(uc, (Q)W::Mc);
+      if (W::Mf != 0.0) Mx = cfmar<Q>(Mx, (Q)W::Mf, sf);
+      CQ sq = ccast<Q, TS>(ps_cur);
+      sq.y = fma(-(Q)alpha_d, sq.x, sq.y);
+      rb = in(b) ? ccast<D, Q>(csub<Q>(ccast<Q, TS>(pf_cur), csub<Q>(Lx, cmul<Q>(sq, Mx)))) : z;
     }
     r2 = r1; r1 = r0; r0 = rb;
     a2 = a1; a1 = a0; a0 = ab;
