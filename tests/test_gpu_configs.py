@@ -76,3 +76,11 @@ def test_config4_replica():
     from paper_2511_16808_b200 import media
     p = media.config_problem(4, scale=16)
     check(*solve_both(p, 3, 0.5, 20, "c64", "element"), "c64")
+
+
+def test_config4_replica_deep():
+    """configs[4] generator at 1/8 scale (96 x 96 x 48 cells, h = 200 m) with a 5-level
+    V-cycle (coarsest 7 x 7 x 4): deep 3D heterogeneous hierarchy (oracle: 37 iterations)."""
+    from paper_2511_16808_b200 import media
+    p = media.config_problem(4, scale=8)
+    check(*solve_both(p, 5, 0.5, 20, "c64", "element"), "c64")
