@@ -161,6 +161,99 @@ __global__ void __launch_bounds__(KRY_THREADS) k_scale(const cplx<TI> *__restric
   }
 }
 
+// c64 variants: two complex values per 16-byte load (float4).  Slab offsets,
+// lengths and the vector stride are multiples of 8 elements (row pitch
+// rounded to 8), so every pair is 16-byte aligned.  len2 = len / 2 pairs.
+template <int NV, bool SELF>
+__global__ void __launch_bounds__(KRY_THREADS) k_multidot_f4(const float4 *__restrict__ V, int64_t vstride2,
+                                                             const float4 *__restrict__ w, int64_t len2,
+                                                             double2 *__restrict__ partial) {
+  constexpr int NA = NV + (SELF ? 1 : 0);
+  double ar[NA], ai[NA];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) ar[i] = ai[i] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len2; e += stride) {
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = V[(int64_t)i * vstride2 + e];
+    const float4 wv = w[e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      ar[i] = fma((double)v[i].x, (double)wv.x, fma((double)v[i].y, (double)wv.y, ar[i]));
+      ai[i] = fma((double)v[i].x, (double)wv.y, fma(-(double)v[i].y, (double)wv.x, ai[i]));
+      ar[i] = fma((double)v[i].z, (double)wv.z, fma((double)v[i].w, (double)wv.w, ar[i]));
+      ai[i] = fma((double)v[i].z, (double)wv.w, fma(-(double)v[i].w, (double)wv.z, ai[i]));
+    }
+    if (SELF) {
+      ar[NV] = fma((double)wv.x, (double)wv.x, fma((double)wv.y, (double)wv.y, ar[NV]));
+      ar[NV] = fma((double)wv.z, (double)wv.z, fma((double)wv.w, (double)wv.w, ar[NV]));
+    }
+  }
+  __shared__ double sr[KRY_THREADS / 32][NA], si[KRY_THREADS / 32][NA];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NA; ++i) {
+    const double a = warp_sum(ar[i]), b = warp_sum(ai[i]);
+    if (lane == 0) { sr[wid][i] = a; si[wid][i] = b; }
+  }
+  __syncthreads();
+  if (threadIdx.x < NA) {
+    double a = 0, b = 0;
+#pragma unroll
+    for (int k = 0; k < KRY_THREADS / 32; ++k) { a += sr[k][threadIdx.x]; b += si[k][threadIdx.x]; }
+    partial[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = make_double2(a, b);
+  }
+}
+
+template <int NV, bool NORM>
+__global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy_f4(const float4 *__restrict__ V, int64_t vstride2,
+                                                               const double2 *__restrict__ coef, const double *vscale,
+                                                               double sgn, float4 *__restrict__ w, int64_t len2,
+                                                               double2 *__restrict__ partial) {
+  __shared__ double2 sc[NV];
+  if (threadIdx.x < NV) {
+    const double f = sgn * (vscale ? vscale[threadIdx.x] : 1.0);
+    sc[threadIdx.x] = make_double2(f * coef[threadIdx.x].x, f * coef[threadIdx.x].y);
+  }
+  __syncthreads();
+  double nrm = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len2; e += stride) {
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = V[(int64_t)i * vstride2 + e];
+    const float4 wv = w[e];
+    double x0 = wv.x, y0 = wv.y, x1 = wv.z, y1 = wv.w;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double2 c = sc[i];
+      x0 = fma(c.x, (double)v[i].x, fma(-c.y, (double)v[i].y, x0));
+      y0 = fma(c.x, (double)v[i].y, fma(c.y, (double)v[i].x, y0));
+      x1 = fma(c.x, (double)v[i].z, fma(-c.y, (double)v[i].w, x1));
+      y1 = fma(c.x, (double)v[i].w, fma(c.y, (double)v[i].z, y1));
+    }
+    const float4 o = make_float4((float)x0, (float)y0, (float)x1, (float)y1);
+    w[e] = o;
+    if (NORM) {
+      nrm = fma((double)o.x, (double)o.x, fma((double)o.y, (double)o.y, nrm));
+      nrm = fma((double)o.z, (double)o.z, fma((double)o.w, (double)o.w, nrm));
+    }
+  }
+  if (NORM) {
+    __shared__ double sn[KRY_THREADS / 32];
+    nrm = warp_sum(nrm);
+    if ((threadIdx.x & 31) == 0) sn[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0;
+#pragma unroll
+      for (int k = 0; k < KRY_THREADS / 32; ++k) a += sn[k];
+      partial[blockIdx.x] = make_double2(a, 0.0);
+    }
+  }
+}
+
 #define HMG_NV_CASES(X) \
   X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
   X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31)

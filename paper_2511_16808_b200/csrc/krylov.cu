@@ -4,6 +4,7 @@
 #include "k_krylov.cuh"
 
 #include <algorithm>
+#include <cstdint>
 #include <mutex>
 #include <unordered_map>
 
@@ -77,9 +78,63 @@ int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef,
   return 0;
 }
 
-template int krylov_multidot<float, float>(int, bool, const float2 *, int64_t, const float2 *, int64_t, double2 *, cudaStream_t);
+// c64 Arnoldi: 16-byte (two complex) loads
+template <>
+int krylov_multidot<float, float>(int nv, bool self, const float2 *V, int64_t vstride, const float2 *w, int64_t len,
+                                  double2 *partial, cudaStream_t s) {
+  if ((len & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15) || (reinterpret_cast<uintptr_t>(w) & 15))
+    throw HmgError(HMG_EINVAL, "multidot: c64 vectors must be 16-byte aligned with even lengths");
+  const dim3 b(KRY_THREADS);
+  const float4 *V4 = reinterpret_cast<const float4 *>(V), *w4 = reinterpret_cast<const float4 *>(w);
+  const int64_t len2 = len / 2, vs2 = vstride / 2;
+  if (self) {
+    switch (nv) {
+#define C_(N) case N: { auto k = k_multidot_f4<N, true>; const int nb = wave_blocks(k, len2); \
+                        launch(k, dim3(nb), b, 0, s, V4, vs2, w4, len2, partial); return nb; }
+      HMG_NV_CASES(C_)
+#undef C_
+    }
+  } else {
+    switch (nv) {
+#define C_(N) case N: { auto k = k_multidot_f4<N, false>; const int nb = wave_blocks(k, len2); \
+                        launch(k, dim3(nb), b, 0, s, V4, vs2, w4, len2, partial); return nb; }
+      HMG_NV_CASES(C_)
+#undef C_
+    }
+  }
+  throw HmgError(HMG_EINVAL, "multidot: vector count out of range");
+  return 0;
+}
+
+template <>
+int krylov_axpy<float, float>(int nv, const float2 *V, int64_t vstride, const double2 *coef, const double *vscale,
+                              double sgn, float2 *w, int64_t len, double2 *partial_norm, cudaStream_t s) {
+  if ((len & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15) || (reinterpret_cast<uintptr_t>(w) & 15))
+    throw HmgError(HMG_EINVAL, "multi_axpy: c64 vectors must be 16-byte aligned with even lengths");
+  const dim3 b(KRY_THREADS);
+  const float4 *V4 = reinterpret_cast<const float4 *>(V);
+  float4 *w4 = reinterpret_cast<float4 *>(w);
+  const int64_t len2 = len / 2, vs2 = vstride / 2;
+  if (partial_norm) {
+    switch (nv) {
+#define C_(N) case N: { auto k = k_multi_axpy_f4<N, true>; const int nb = wave_blocks(k, len2); \
+                        launch(k, dim3(nb), b, 0, s, V4, vs2, coef, vscale, sgn, w4, len2, partial_norm); return nb; }
+      HMG_NV_CASES(C_)
+#undef C_
+    }
+  } else {
+    switch (nv) {
+#define C_(N) case N: { auto k = k_multi_axpy_f4<N, false>; const int nb = wave_blocks(k, len2); \
+                        launch(k, dim3(nb), b, 0, s, V4, vs2, coef, vscale, sgn, w4, len2, (double2 *)nullptr); return nb; }
+      HMG_NV_CASES(C_)
+#undef C_
+    }
+  }
+  throw HmgError(HMG_EINVAL, "multi_axpy: vector count out of range");
+  return 0;
+}
+
 template int krylov_multidot<double, double>(int, bool, const double2 *, int64_t, const double2 *, int64_t, double2 *, cudaStream_t);
-template int krylov_axpy<float, float>(int, const float2 *, int64_t, const double2 *, const double *, double, float2 *, int64_t, double2 *, cudaStream_t);
 template int krylov_axpy<double, double>(int, const double2 *, int64_t, const double2 *, const double *, double, double2 *, int64_t, double2 *, cudaStream_t);
 template int krylov_axpy<float, double>(int, const float2 *, int64_t, const double2 *, const double *, double, double2 *, int64_t, double2 *, cudaStream_t);
 

@@ -72,6 +72,14 @@ Comm *local_comm_create(const std::shared_ptr<void> &group, int rank);
 void nccl_unique_id(void *out128);
 Comm *nccl_comm_create(const void *uid, int rank, int n);
 
+// c64 Arnoldi kernels use 16-byte loads (explicit specialisations in krylov.cu)
+template <>
+int krylov_multidot<float, float>(int nv, bool self, const float2 *V, int64_t vstride, const float2 *w, int64_t len,
+                                  double2 *partial, cudaStream_t s);
+template <>
+int krylov_axpy<float, float>(int nv, const float2 *V, int64_t vstride, const double2 *coef, const double *vscale,
+                              double sgn, float2 *w, int64_t len, double2 *partial_norm, cudaStream_t s);
+
 // Fused Galerkin-level Vanka sweep, 2D (smooth2d.cu).
 // hinv == nullptr: patches factored on the fly in every sweep; else the
 // stored patch inverses are applied.

@@ -1,2 +1,3 @@
 set -x
-timeout 1500 python scripts/deep_probe3.py > gpurun_out/deep3.log 2>&1; echo exit=$? >> gpurun_out/deep3.log
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_exit=$? >> gpurun_out/bench.err
