@@ -80,6 +80,67 @@ __global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<TS> *__restri
   y[i] = ccast<T, TC>(f ? csub<TC>(ccast<TC, T>(f[i]), Ax) : Ax);
 }
 
+// 2D c64 variant of k_fine_op: one thread per PAIR of x-adjacent nodes
+// (x0 = 2p, x0 + 1), 16-byte loads of the pairs (interior x offset G and row
+// pitch are even, so pairs are aligned).  Same arithmetic per node as
+// k_fine_op; the second node of the last pair of an odd row is a ghost and is
+// not written.  TSG = storage of sigma (float2 or double2).
+template <int KIND, typename TC, typename TSG>
+__global__ void __launch_bounds__(256) k_fine_op2d_pair(Geo g, const cplx<TSG> *__restrict__ sig, TC alpha, TC ih2,
+                                                        const float2 *__restrict__ x, const float2 *__restrict__ f,
+                                                        float2 *__restrict__ y) {
+  using W = FineW<2, KIND>;
+  using CC = cplx<TC>;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
+  const int x0 = 2 * p;
+  if (x0 >= g.n[0] || iy >= g.n[1]) return;
+  const int64_t i = g.idx(x0, iy, 0);
+  const int64_t px = g.px;
+  auto row = [&](int64_t c, CC &l, CC &a, CC &b, CC &r) {   // x[c-1], x[c], x[c+1], x[c+2]
+    const float4 ab = *reinterpret_cast<const float4 *>(x + c);
+    const float2 lv = x[c - 1], rv = x[c + 2];
+    l = mkc<TC>(lv.x, lv.y);
+    a = mkc<TC>(ab.x, ab.y);
+    b = mkc<TC>(ab.z, ab.w);
+    r = mkc<TC>(rv.x, rv.y);
+  };
+  CC nl, na, nb, nr, cl, ca, cb, cr, sl, sa, sb, sr;
+  row(i - px, nl, na, nb, nr);
+  row(i, cl, ca, cb, cr);
+  row(i + px, sl, sa, sb, sr);
+  // node x0 (a) and node x0 + 1 (b)
+  const CC sfa = cadd<TC>(cadd<TC>(cl, cb), cadd<TC>(na, sa));
+  const CC sfb = cadd<TC>(cadd<TC>(ca, cr), cadd<TC>(nb, sb));
+  CC La = cscale<TC>(ca, (TC)W::Lc), Lb = cscale<TC>(cb, (TC)W::Lc);
+  La = cfmar<TC>(La, (TC)W::Lf, sfa);
+  Lb = cfmar<TC>(Lb, (TC)W::Lf, sfb);
+  if (W::Le != 0.0) {
+    La = cfmar<TC>(La, (TC)W::Le, cadd<TC>(cadd<TC>(nl, nb), cadd<TC>(sl, sb)));
+    Lb = cfmar<TC>(Lb, (TC)W::Le, cadd<TC>(cadd<TC>(na, nr), cadd<TC>(sa, sr)));
+  }
+  La = cscale<TC>(La, ih2);
+  Lb = cscale<TC>(Lb, ih2);
+  CC Ma = cscale<TC>(ca, (TC)W::Mc), Mb = cscale<TC>(cb, (TC)W::Mc);
+  if (W::Mf != 0.0) {
+    Ma = cfmar<TC>(Ma, (TC)W::Mf, sfa);
+    Mb = cfmar<TC>(Mb, (TC)W::Mf, sfb);
+  }
+  CC sga = ccast<TC, TSG>(sig[i]), sgb = ccast<TC, TSG>(sig[i + 1]);
+  sga.y = fma(-alpha, sga.x, sga.y);
+  sgb.y = fma(-alpha, sgb.x, sgb.y);
+  CC oa = csub<TC>(La, cmul<TC>(sga, Ma)), ob = csub<TC>(Lb, cmul<TC>(sgb, Mb));
+  if (f) {
+    const float4 fv = *reinterpret_cast<const float4 *>(f + i);
+    oa = csub<TC>(mkc<TC>(fv.x, fv.y), oa);
+    ob = csub<TC>(mkc<TC>(fv.z, fv.w), ob);
+  }
+  if (x0 + 1 < g.n[0])
+    *reinterpret_cast<float4 *>(y + i) = make_float4((float)oa.x, (float)oa.y, (float)ob.x, (float)ob.y);
+  else
+    y[i] = make_float2((float)oa.x, (float)oa.y);
+}
+
 // Stored stencil of radius R: coef[k][j], k = (ox+R) + (2R+1)((oy+R) + (2R+1)(oz+R)),
 // multiplies x[j + o].  Coefficients towards out-of-domain nodes are zero.
 // TV = vector storage/arithmetic (fp64 on Galerkin levels), TK = coefficient storage.
