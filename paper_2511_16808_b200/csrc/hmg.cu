@@ -717,8 +717,8 @@ template <typename T> struct Solver : SolverBase {
         if (c4) launch(k_rb2d_march<T, ST_COMPACT4, true, SEG, double, double>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
         else launch(k_rb2d_march<T, ST_FD2, true, SEG, double, double>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
       } else {
-        if (c4) launch(k_rb2d_march<T, ST_COMPACT4, false, SEG, double, double>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
-        else launch(k_rb2d_march<T, ST_FD2, false, SEG, double, double>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        if (c4) launch(k_rb2d_march<T, ST_COMPACT4, false, SEG, double, T>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        else launch(k_rb2d_march<T, ST_FD2, false, SEG, double, T>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
       }
       return;
     }

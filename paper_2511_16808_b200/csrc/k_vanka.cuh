@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__
     pa = lr(ia_, b + 1);
     pid = lr(id_, b);
     if (!ZERO) ps = lr(sig, b + 1);
-    // ---- r(b) in TR, t(b)
+    // ---- r(b) in TR, t(b).  L u in difference form, sum w (u_nb - u_c): exact
+    // algebra because Lc + 4 Lf + 4 Le = 0 (zero ghosts included), and it keeps
+    // the cancellation of the compact stencil out of a low-precision sum.
     CD rb = fb;
     if (!ZERO) {
       using Q = TR;
@@ -231,11 +233,15 @@ __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__
                                : mkc<TS>(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1)));
       };
       const CQ uc = ccast<Q, TS>(u0);
-      const CQ sf = cadd<Q>(cadd<Q>(sh(u0, true), sh(u0, false)), cadd<Q>(ccast<Q, TS>(um1), ccast<Q, TS>(up1)));
-      CQ Lx = cscale<Q>(uc, (Q)W::Lc);
-      Lx = cfmar<Q>(Lx, (Q)W::Lf, sf);
-      if (W::Le != 0.0)
-        Lx = cfmar<Q>(Lx, (Q)W::Le, cadd<Q>(cadd<Q>(sh(um1, true), sh(um1, false)), cadd<Q>(sh(up1, true), sh(up1, false))));
+      const CQ un = ccast<Q, TS>(um1), us = ccast<Q, TS>(up1), uw = sh(u0, true), ue = sh(u0, false);
+      const CQ sf = cadd<Q>(cadd<Q>(uw, ue), cadd<Q>(un, us));
+      CQ dlt = cadd<Q>(cadd<Q>(csub<Q>(uw, uc), csub<Q>(ue, uc)), cadd<Q>(csub<Q>(un, uc), csub<Q>(us, uc)));
+      CQ Lx = cscale<Q>(dlt, (Q)W::Lf);
+      if (W::Le != 0.0) {
+        const CQ d2 = cadd<Q>(cadd<Q>(csub<Q>(sh(um1, true), uc), csub<Q>(sh(um1, false), uc)),
+                              cadd<Q>(csub<Q>(sh(up1, true), uc), csub<Q>(sh(up1, false), uc)));
+        Lx = cfmar<Q>(Lx, (Q)W::Le, d2);
+      }
       Lx = cscale<Q>(Lx, (Q)ih2_d);
       CQ Mx = cscale<Q>(uc, (Q)W::Mc);
       if (W::Mf != 0.0) Mx = cfmar<Q>(Mx, (Q)W::Mf, sf);
