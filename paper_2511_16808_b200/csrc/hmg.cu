@@ -12,6 +12,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -32,6 +33,8 @@ namespace hmg {
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count_now() { return g_launches.load(); }
+void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // ---- opt-in per-kernel profiling (hmg_profile_begin / hmg_profile_report)
 struct ProfRec {
@@ -46,6 +49,7 @@ struct Profiler {
   size_t used = 0;
 };
 static Profiler g_prof;
+bool prof_active() { return g_prof.on; }
 static thread_local const char *t_name = nullptr;
 static thread_local int t_level = 0;
 static thread_local double t_bytes = 0;
@@ -245,11 +249,21 @@ template <typename T> struct Solver : SolverBase {
   DBuf V, Z, partial, dres, io;
   DBuf qd, xd, rd;        // fp64 right-hand side, iterate and restart residual
   int reorth = 0;         // second Gram-Schmidt passes in the last solve
+  // CUDA graph of the coarse part of the cycle (levels >= 1 run on fixed
+  // buffers, so one capture serves every call); single-rank runs only
+  cudaGraphExec_t cgraph = nullptr;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  long long cgraph_kernels = 0;
   int nblk = 0;
   double *hpin = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   ~Solver() override {
+    if (cgraph) cudaGraphExecDestroy(cgraph);
+    if (gev_in) cudaEventDestroy(gev_in);
+    if (gev_out) cudaEventDestroy(gev_out);
+    if (gstream) cudaStreamDestroy(gstream);
     if (hpin) cudaFreeHost(hpin);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -763,8 +777,42 @@ template <typename T> struct Solver : SolverBase {
            (const D *)r, (D *)e);
   }
 
+  bool graphs_ok() const { return (!comm || comm->size == 1) && !prof_active() && std::getenv("HMG_NO_GRAPHS") == nullptr; }
+
+  // levels >= 1 of the cycle (zero initial guess on lev[1].u, rhs lev[1].f)
+  // as one CUDA graph launch, on a private stream ordered against the caller's
+  // stream by events (the legacy default stream cannot be captured)
+  void coarse_cycle_graph(cudaStream_t s) {
+    if (!gstream) {
+      CK(cudaStreamCreateWithFlags(&gstream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&gev_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&gev_out, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(gev_in, s));
+    CK(cudaStreamWaitEvent(gstream, gev_in, 0));
+    if (!cgraph) {
+      const long long k0 = launch_count_now();
+      cudaGraph_t gr;
+      CK(cudaStreamBeginCapture(gstream, cudaStreamCaptureModeThreadLocal));
+      cycle(1, lev[1].f.p, lev[1].u.p, 1, gstream, true);
+      CK(cudaStreamEndCapture(gstream, &gr));
+      CK(cudaGraphInstantiate(&cgraph, gr, 0));
+      CK(cudaGraphDestroy(gr));
+      cgraph_kernels = launch_count_now() - k0;
+      add_launches(-cgraph_kernels);          // captured, not launched
+    }
+    CK(cudaGraphLaunch(cgraph, gstream));
+    add_launches(cgraph_kernels);
+    CK(cudaEventRecord(gev_out, gstream));
+    CK(cudaStreamWaitEvent(s, gev_out, 0));
+  }
+
   // Alg. 2.1, recursive; u <- MG_l(f, u)
-  void cycle(int l, const void *f, void *u, int zero, cudaStream_t s) {
+  void cycle(int l, const void *f, void *u, int zero, cudaStream_t s, bool capturing = false) {
+    if (l == 1 && zero && !capturing && L > 2 && f == lev[1].f.p && u == lev[1].u.p && graphs_ok()) {
+      coarse_cycle_graph(s);
+      return;
+    }
     if (l == L - 1) {
       coarse_(f, u, s);
       return;
@@ -779,7 +827,7 @@ template <typename T> struct Solver : SolverBase {
     Level &Cc = lev[l + 1];
     restrict_(l, Lv.r_.p, Cc.f.p, s);                          //         f_c = R r
     const int rec = opt.cycle == 1 ? 2 : 1;                    // step 3: V / W recursion
-    for (int c = 0; c < rec; ++c) cycle(l + 1, Cc.f.p, Cc.u.p, c == 0, s);
+    for (int c = 0; c < rec; ++c) cycle(l + 1, Cc.f.p, Cc.u.p, c == 0, s, capturing);
     if (opt.nu2 > 0 && fused_sweep(l)) {
       prolong_(l, Cc.u.p, u, Lv.r_.p, s);                      // step 4: S = u + P e (r_ is free now)
       smooth(l, f, Lv.r_.p, u, 0, s);                          // step 5: u = S + w B (f - A S)

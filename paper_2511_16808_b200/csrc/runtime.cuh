@@ -29,6 +29,9 @@ struct HmgError : std::runtime_error {
 // Tag the next launch with its kernel class, level and ALGORITHMIC bytes
 // (DESIGN.md §5); consumed by launch() when profiling is on.
 void tag(const char *name, int level, double bytes);
+bool prof_active();
+long long launch_count_now();
+void add_launches(long long n);
 int prof_before(cudaStream_t s);
 void prof_after(cudaStream_t s, int idx);
 
