@@ -522,6 +522,19 @@ template <typename T> struct Solver : SolverBase {
     if (comm && comm->size > 1) comm->allreduce_sum(reinterpret_cast<double *>(d), 2 * n, s);
   }
 
+  // level 1 of a 2D Galerkin hierarchy: residual/apply through the fine grid
+  // (opt-in, HMG_MF1=1: measured 0.33 ms vs 0.19 ms for the stored stencil at
+  // N = 4096, shared-memory-wavefront bound).
+  // Slabs: the coarse slab's R P support, fine rows [2 lo - rR - 1, 2 (hi - 1) + rR + 1],
+  // must lie inside the fine slab's ghosted rows (sigma is sliced with G ghost rows).
+  bool mf_level1(int l) const {
+    if (l != 1 || L < 2 || opt.dim != 2 || opt.coarse_op != HMG_GALERKIN || !std::getenv("HMG_MF1")) return false;
+    const Level &F = lev[0], &C1 = lev[1];
+    if (!F.dist) return true;
+    if (!C1.dist) return false;
+    return 2 * C1.lo - F.rR - 1 >= F.lo - G && 2 * (C1.hi - 1) + F.rR + 1 < F.hi + G;
+  }
+
   // 2D c64 fine level with an even ghost width: node pairs are 16-byte aligned
   // (used for the FGMRES matvec; measured: the scalar kernel is faster for the
   // V-cycle residual, whose sigma is fp32)
@@ -606,9 +619,36 @@ template <typename T> struct Solver : SolverBase {
       }
       return;
     }
-    const C *cf = Lv.coef.template as<C>();
     const D *xx = (const D *)x, *ff = (const D *)f;
     D *yy = (D *)y;
+    if (mf_level1(l)) {   // A_1 = R_0 H_s P_0 through the fine grid (no coefficient planes)
+      const Level &F = lev[0];
+      constexpr int TX = 32, TY = 8;
+      const dim3 block(32, 8), grid((Lv.geo.n[0] + TX - 1) / TX, (Lv.geo.n[1] + TY - 1) / TY);
+      tag(f ? "mf_residual" : "mf_apply", l, (f ? 3 : 2) * sizeof(D) * nn + 4 * sizeof(D) * nn);
+      const D *sg = sigd.template as<D>();
+      const double ih2 = 1.0 / (F.h * F.h);
+      const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+      auto go = [&](auto kern, int smem) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        launch(kern, grid, block, (size_t)smem, s, F.geo, Lv.geo, sg, alpha, ih2, xx, ff, yy);
+      };
+      // fp64 tile arithmetic (fp32 tiles measured: config 0 c64 35 FGMRES iterations vs 30)
+#define HMG_MF1(KIND, RR, PR) go(k_galerkin1_mf<double, KIND, RR, PR, TX, TY, double>, MF1Tile<RR, TX, TY, 16>::SMEM)
+      if (F.rR == 2 && F.rP == 2) {
+        if (c4) HMG_MF1(ST_COMPACT4, 2, 2);
+        else HMG_MF1(ST_FD2, 2, 2);
+      } else if (F.rR == 1 && F.rP == 1) {
+        if (c4) HMG_MF1(ST_COMPACT4, 1, 1);
+        else HMG_MF1(ST_FD2, 1, 1);
+      } else {
+        if (c4) HMG_MF1(ST_COMPACT4, 1, 2);
+        else HMG_MF1(ST_FD2, 1, 2);
+      }
+#undef HMG_MF1
+      return;
+    }
+    const C *cf = Lv.coef.template as<C>();
     tag(f ? "stored_residual" : "stored_apply", l,
         kcount(opt.dim, Lv.r) * sizeof(C) * nn + (f ? 3 : 2) * sz * nn);
     if (opt.dim == 2) {

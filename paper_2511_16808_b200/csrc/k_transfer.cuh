@@ -163,4 +163,163 @@ __global__ void __launch_bounds__(256) k_prolong_block(Geo gf, Geo gc, int cx0, 
       }
 }
 
+// Level-1 operator of the Galerkin hierarchy evaluated MATRIX-FREE through the
+// fine grid (2D):  A_1 u = R_0 (L - diag(sigma_s) M) P_0 u, i.e.
+// y = A_1 u  or  y = f - A_1 u, with t = P u and s = H_s t formed on the fine
+// tile in shared memory.  Truncation is exact: t and s vanish outside the
+// domain (P and R have no rows there), L and M read those zeros.  Reads u and f
+// on the coarse tile and sigma on the fine tile: 2-3 vectors + 4 sigma values
+// per coarse node instead of the (2r+1)^2 stored coefficient planes.
+// Both transfers are applied separably (x pass, then y pass) with 3 / 2RR+1
+// branch-free taps (odd fine nodes take weight 0 on their first tap).
+// Shared memory (dynamic): region A = {u tile, P_x u} then s; region B = t,
+// then R_x s.  f and the tile's sigma are prefetched into registers.
+template <int PR, typename T>
+__device__ __forceinline__ void ptaps3(int x, int &c, int &d0, T &w0, T &w1, T &w2) {
+  // fine x -> coarse taps (c + d0, c, c + 1) with weights w0..w2; every tap address
+  // lies in the coarse support of x (odd x: d0 = 0 with w0 = 0), so no read leaves the tile
+  c = x >> 1;   // floor
+  const bool odd = x & 1;
+  if (PR == 2) {
+    d0 = odd ? 0 : -1;
+    w0 = odd ? T(0) : T(0.125);
+    w1 = odd ? T(0.5) : T(0.75);
+    w2 = odd ? T(0.5) : T(0.125);
+  } else {
+    d0 = 0;
+    w0 = T(0);
+    w1 = odd ? T(0.5) : T(1);
+    w2 = odd ? T(0.5) : T(0);
+  }
+}
+
+template <int RR, int TX, int TY, int WB = 16>
+struct MF1Tile {
+  static constexpr int CX = TX + 4, CY = TY + 4;                        // coarse u (tile + 2)
+  static constexpr int FX = 2 * TX + 2 * RR - 1, FY = 2 * TY + 2 * RR - 1;   // s (R support)
+  static constexpr int TXF = FX + 2, TYF = FY + 2;                      // t (+1 ring)
+  static constexpr int A_WORDS = (CX * CY + TXF * CY) > FX * FY ? (CX * CY + TXF * CY) : FX * FY;
+  static constexpr int B_WORDS = TXF * TYF > TX * FY ? TXF * TYF : TX * FY;
+  static constexpr int SMEM = (A_WORDS + B_WORDS) * WB;
+  static constexpr int NS = (FX * FY + 255) / 256;
+};
+
+// TC: tile arithmetic precision (double, or float for the c64 path: the
+// stored-coefficient alternative carries fp32-rounded coefficients anyway);
+// u, f, y are fp64 coarse vectors, the final f - A u is formed in fp64.
+template <typename TSG, int KIND, int RR, int PR, int TX, int TY, typename TC = double>
+__global__ void __launch_bounds__(256) k_galerkin1_mf(Geo gf, Geo gc, const cplx<TSG> *__restrict__ sig, double alpha,
+                                                      double ih2, const double2 *__restrict__ u,
+                                                      const double2 *__restrict__ f, double2 *__restrict__ y) {
+  using T = TC;
+  using V = cplx<TC>;
+  using W = FineW<2, KIND>;
+  using Tl = MF1Tile<RR, TX, TY, sizeof(V)>;
+  constexpr int NT = 256, CX = Tl::CX, CY = Tl::CY, FX = Tl::FX, FY = Tl::FY, TXF = Tl::TXF, TYF = Tl::TYF;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V *smem = reinterpret_cast<V *>(smem_raw);
+  V *su = smem;                  // [CY][CX]     phase 0-1
+  V *sx = su + CX * CY;          // [CY][TXF]    phase 1-2  (P_x u)
+  V *ss = smem;                  // [FY][FX]     phase 3-4  (aliases su, sx)
+  V *st = smem + Tl::A_WORDS;    // [TYF][TXF]   phase 2-3
+  V *sr = st;                    // [FY][TX]     phase 4-5  (R_x s, aliases st)
+  const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;   // coarse-local tile origin
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const V zero = mkc<T>(0, 0);
+  const int cx0 = X0 + gc.o[0] - 2, cy0 = Y0 + gc.o[1] - 2;                   // global coarse origin of su
+  const int fx0 = 2 * (X0 + gc.o[0]) - RR, fy0 = 2 * (Y0 + gc.o[1]) - RR;   // global fine origin of ss
+  // prefetch: f of this thread's output node, sigma of its s nodes
+  const int ox = threadIdx.x, oy = threadIdx.y;
+  const bool own = X0 + ox < gc.n[0] && Y0 + oy < gc.n[1];
+  const int64_t io = own ? gc.idx(X0 + ox, Y0 + oy, 0) : 0;
+  double2 fv = make_double2(0, 0);
+  if (f && own) fv = f[io];
+  cplx<TSG> sg[Tl::NS];
+#pragma unroll
+  for (int k = 0; k < Tl::NS; ++k) {
+    const int i = tid + k * NT;
+    const int fx = fx0 + i % FX, fy = fy0 + i / FX;
+    sg[k] = mkc<TSG>(0, 0);
+    if (i < FX * FY && fx >= 0 && fx < gf.N[0] && fy >= 0 && fy < gf.N[1])
+      sg[k] = sig[gf.idx(fx - gf.o[0], fy - gf.o[1], 0)];
+  }
+  for (int i = tid; i < CX * CY; i += NT) {
+    const int gx = cx0 + i % CX, gy = cy0 + i / CX;
+    const bool in = gx >= 0 && gx < gc.N[0] && gy >= 0 && gy < gc.N[1];
+    su[i] = in ? ccast<T, double>(u[gc.idx(gx - gc.o[0], gy - gc.o[1], 0)]) : zero;
+  }
+  __syncthreads();
+  // phase 1: sx = P_x u on coarse rows, fine columns fx0-1 .. fx0+FX
+  for (int i = tid; i < CY * TXF; i += NT) {
+    const int r = i / TXF, lx = i % TXF;
+    int c, d0;
+    T w0, w1, w2;
+    ptaps3<PR>(fx0 - 1 + lx, c, d0, w0, w1, w2);
+    const V *row = su + r * CX + (c - cx0);
+    V acc = cscale<T>(row[d0], w0);
+    acc = cfmar<T>(acc, w1, row[0]);
+    acc = cfmar<T>(acc, w2, row[1]);
+    sx[i] = acc;
+  }
+  __syncthreads();
+  // phase 2: t = P_y sx, zero outside the domain
+  for (int i = tid; i < TYF * TXF; i += NT) {
+    const int ly = i / TXF, lx = i % TXF;
+    const int fx = fx0 - 1 + lx, fy = fy0 - 1 + ly;
+    int c, d0;
+    T w0, w1, w2;
+    ptaps3<PR>(fy, c, d0, w0, w1, w2);
+    const V *col = sx + (c - cy0) * TXF + lx;
+    V acc = cscale<T>(col[d0 * TXF], w0);
+    acc = cfmar<T>(acc, w1, col[0]);
+    acc = cfmar<T>(acc, w2, col[TXF]);
+    const bool in = fx >= 0 && fx < gf.N[0] && fy >= 0 && fy < gf.N[1];
+    st[i] = in ? acc : zero;
+  }
+  __syncthreads();
+  // phase 3: s = (L - sigma_s M) t (sigma = 0 outside the domain and t = 0 there: s = 0 only
+  // if also L t = 0, so mask explicitly)
+#pragma unroll
+  for (int k = 0; k < Tl::NS; ++k) {
+    const int i = tid + k * NT;
+    if (i < FX * FY) {
+      const int lx = i % FX, ly = i / FX;
+      const int fx = fx0 + lx, fy = fy0 + ly;
+      const V *c = st + (ly + 1) * TXF + (lx + 1);
+      const V sf = cadd<T>(cadd<T>(c[-1], c[1]), cadd<T>(c[-TXF], c[TXF]));
+      V Lx = cscale<T>(c[0], (T)W::Lc);
+      Lx = cfmar<T>(Lx, (T)W::Lf, sf);
+      if (W::Le != 0.0)
+        Lx = cfmar<T>(Lx, (T)W::Le, cadd<T>(cadd<T>(c[-TXF - 1], c[-TXF + 1]), cadd<T>(c[TXF - 1], c[TXF + 1])));
+      Lx = cscale<T>(Lx, (T)ih2);
+      V Mx = cscale<T>(c[0], (T)W::Mc);
+      if (W::Mf != 0.0) Mx = cfmar<T>(Mx, (T)W::Mf, sf);
+      V sv = ccast<T, TSG>(sg[k]);
+      sv.y = fma((T)-alpha, sv.x, sv.y);
+      const bool in = fx >= 0 && fx < gf.N[0] && fy >= 0 && fy < gf.N[1];
+      ss[i] = in ? csub<T>(Lx, cmul<T>(sv, Mx)) : zero;
+    }
+  }
+  __syncthreads();
+  // phase 4: sr = R_x s  (row ly, coarse column ox)
+  for (int i = tid; i < FY * TX; i += NT) {
+    const int ly = i / TX, c = i % TX;
+    const V *row = ss + ly * FX + 2 * c;
+    V acc = zero;
+#pragma unroll
+    for (int k = 0; k <= 2 * RR; ++k) acc = cfmar<T>(acc, (T)RW<RR>::w(k - RR), row[k]);
+    sr[i] = acc;
+  }
+  __syncthreads();
+  // phase 5: y = R_y sr
+  if (own) {
+    const V *col = sr + 2 * oy * TX + ox;
+    V acc = zero;
+#pragma unroll
+    for (int k = 0; k <= 2 * RR; ++k) acc = cfmar<T>(acc, (T)RW<RR>::w(k - RR), col[k * TX]);
+    const double2 ad = ccast<double, T>(acc);
+    y[io] = f ? csub<double>(fv, ad) : ad;
+  }
+}
+
 }  // namespace hmg

@@ -2,6 +2,7 @@
 
     python scripts/ncu_summary.py launches gpurun_out/launches.csv profiles/r01_launches.md
     python scripts/ncu_summary.py full gpurun_out/prof.ncu-rep profiles/r01_ncu_full.md [--traffic-key NAME]
+        [--traffic-kernel SUBSTRING]   (largest per-launch DRAM bytes among kernels matching SUBSTRING)
 
 `launches`: the `--metrics gpu__time_duration.sum` launch list (cold-cache,
 serialised: compare SHARES, not absolute times) aggregated per kernel.
@@ -68,7 +69,7 @@ STALLS = ["long_scoreboard", "barrier", "short_scoreboard", "wait", "math_pipe_t
           "lg_throttle", "not_selected", "selected", "no_instruction", "dispatch_stall", "drain", "membar"]
 
 
-def full(src, dst, traffic_key=None):
+def full(src, dst, traffic_key=None, traffic_kernel=None):
     raw = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -103,7 +104,8 @@ def full(src, dst, traffic_key=None):
     if traffic_key:
         tf = os.path.join(os.path.dirname(dst), "ncu_traffic.json")
         cur = json.load(open(tf)) if os.path.exists(tf) else {}
-        best = max(traffic.values(), key=lambda v: max(v)) if traffic else None
+        cand = [v for k, v in traffic.items() if not traffic_kernel or traffic_kernel in k]
+        best = max(cand, key=lambda v: max(v)) if cand else None
         if best:
             cur[traffic_key] = max(best)
         json.dump(cur, open(tf, "w"), indent=1)
@@ -116,5 +118,9 @@ def _scale(unit):
 if __name__ == "__main__":
     kind, src, dst = sys.argv[1:4]
     key = sys.argv[sys.argv.index("--traffic-key") + 1] if "--traffic-key" in sys.argv else None
+    kk = sys.argv[sys.argv.index("--traffic-kernel") + 1] if "--traffic-kernel" in sys.argv else None
     os.makedirs(os.path.dirname(dst) or ".", exist_ok=True)
-    (launches if kind == "launches" else full)(*([src, dst] + ([key] if kind == "full" else [])))
+    if kind == "launches":
+        launches(src, dst)
+    else:
+        full(src, dst, key, kk)
