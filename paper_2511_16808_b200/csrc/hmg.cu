@@ -771,8 +771,10 @@ template <typename T> struct Solver : SolverBase {
         if (c4) launch(k_rb2d_march<T, ST_COMPACT4, true, SEG, double, double>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
         else launch(k_rb2d_march<T, ST_FD2, true, SEG, double, double>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
       } else {
-        if (c4) launch(k_rb2d_march<T, ST_COMPACT4, false, SEG, double, T>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
-        else launch(k_rb2d_march<T, ST_FD2, false, SEG, double, T>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        // c64: 3 blocks/SM (80 registers, 24 B spill) measured 16 % faster than 2 (91 registers)
+        constexpr int MB = sizeof(T) == 4 ? 3 : 2;
+        if (c4) launch(k_rb2d_march<T, ST_COMPACT4, false, SEG, double, T, 1, MB>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        else launch(k_rb2d_march<T, ST_FD2, false, SEG, double, T, 1, MB>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
       }
       return;
     }

@@ -65,12 +65,20 @@ template <int DIM, int KIND> struct Patch {
   }
 };
 
+// 1 / cnt_j for cnt_j = 1..8 (a table instead of a per-node fp64 division)
+__constant__ double kInvCount[9] = {0.0, 1.0, 0.5, 1.0 / 3.0, 0.25, 0.2, 1.0 / 6.0, 1.0 / 7.0, 0.125};
+
 // (1a) generic sweep with stored inverses, as a direct gather (any dim/kind):
 //   u_out_j = u_j + (w/cnt_j) sum_{s: anchor c = j - o_s} sum_q Hinv_c[s][q] r[c + o_q]
 // (r = f - A u precomputed; r = f for a zero initial guess).  Only row s of
 // each containing anchor's inverse is read, so every stored entry is read once
 // per sweep and no patch solution is staged.  Each node reads/writes only its
-// own u: in place is safe.
+// own u: in place is safe.  Branch-free: a position c = j - o_s that is not an
+// anchor (outside the domain, or an Element corner on the far faces) holds an
+// all-zero inverse (buffers are zeroed at allocation, k_patch_inverse writes
+// anchors only; slab ghost rows hold the neighbour's anchors), and r is finite
+// there (zero ghosts / exchanged halo), so its terms vanish exactly and every
+// load of the node can be in flight at once.
 template <typename T, typename TK, int DIM, int KIND>
 __global__ void __launch_bounds__(256) k_vanka_direct(Geo g, const cplx<TK> *__restrict__ hinv,
                                                       const cplx<T> *__restrict__ r, const cplx<T> *u,
@@ -83,7 +91,6 @@ __global__ void __launch_bounds__(256) k_vanka_direct(Geo g, const cplx<TK> *__r
   for (int sI = 0; sI < K; ++sI) {
     int dx, dy, dz;
     P::off(sI, dx, dy, dz);
-    if (!P::anchor(g, ix - dx, iy - dy, iz - dz)) continue;
     const int64_t c = g.idx(ix - dx, iy - dy, iz - dz);
     cplx<TK> hw[K];
 #pragma unroll
@@ -96,7 +103,7 @@ __global__ void __launch_bounds__(256) k_vanka_direct(Geo g, const cplx<TK> *__r
     }
   }
   const int64_t j = g.idx(ix, iy, iz);
-  const cplx<T> upd = cscale<T>(acc, w / (T)P::count(g, ix, iy, iz));
+  const cplx<T> upd = cscale<T>(acc, w * (T)kInvCount[P::count(g, ix, iy, iz)]);
   u_out[j] = zero ? upd : cadd<T>(u[j], upd);
 }
 
@@ -156,13 +163,18 @@ __device__ __forceinline__ float2 shfl_dn1(float2 v) {
 }
 
 constexpr int RB_STRIP = 26;
+// count-dependent factors of the RB gather: k (number of present diagonal
+// anchors) as a double and 1 / (1 + k)  (a table instead of I2F + a division)
+__constant__ double kRbCount[5] = {0.0, 1.0, 2.0, 3.0, 4.0};
+__constant__ double kRbInvCnt[5] = {1.0, 0.5, 1.0 / 3.0, 0.25, 0.2};
 
 // Out of place: u_out = u_in + w B (f - H_s u_in) (u_in unused with ZERO).  In
 // place would race: other warps still read old u in their halo rows/columns.
 // TC = arithmetic precision of the patch algebra (fp64, or the storage
 // precision), TR = precision of the residual f - H_s u
-template <typename TS, int KIND, bool ZERO, int SEG, typename TC = double, typename TR = double>
-__global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__restrict__ sig,
+template <typename TS, int KIND, bool ZERO, int SEG, typename TC = double, typename TR = double, int UNR = 1,
+          int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> *__restrict__ sig,
                                                     const cplx<TS> *__restrict__ ia_, const cplx<TS> *__restrict__ id_,
                                                     double alpha_d, double ih2_d, const cplx<TS> *__restrict__ f,
                                                     const cplx<TS> *__restrict__ u, cplx<TS> *__restrict__ u_out,
@@ -193,34 +205,42 @@ __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__
   CS um1 = zs, u0 = zs, up1 = zs;       // u at rows b-1, b, b+1
   CS ub1 = zs;                          // u at row b-2 (the output row)
   CD r2 = z, r1 = z, r0 = z;            // r at rows b-2, b-1, b
-  CD t2 = z, t1 = z, t0 = z;            // t = r ia at rows b-2, b-1, b
+  CD h2 = z, h1 = z, h0 = z;            // horizontal sums t(x-1) + t(x+1) of t = r ia, rows b-2, b-1, b
   CS a2 = zs, a1 = zs, a0 = zs;         // ia at rows b-2, b-1, b
-  CD c3 = z, c2 = z, c1 = z;            // y_c at rows b-3, b-2, b-1
+  CD c2 = z, c1 = z;                    // y_c at rows b-2, b-1
+  CD g3 = z, g2 = z, g1 = z;            // horizontal sums y_c(x-1) + y_c(x+1), rows b-3, b-2, b-1
   // one-step-ahead prefetch registers, kept in the storage type so that the
   // loads of step b+1 stay in flight during step b
   // per-lane column offset; row y of array a sits at a + col + y * px
-  const int64_t col = g.base + x;
   const int64_t px = g.px;
-  auto lr = [&](const CS *a, int y) { return in(y) ? a[col + (int64_t)y * px] : zs; };
+  // running element offset of row b in this lane's column (one 64-bit add per row)
+  int64_t ob = g.base + x + (int64_t)(y0 - 2) * px;
+  auto lr = [&](const CS *a, int y, int64_t o) { return in(y) ? a[o] : zs; };
   if (!ZERO) {
-    u0 = lr(u, y0 - 3);
-    up1 = lr(u, y0 - 2);
+    u0 = lr(u, y0 - 3, ob - px);
+    up1 = lr(u, y0 - 2, ob);
   }
-  CS pu = ZERO ? zs : lr(u, y0 - 1), pf = lr(f, y0 - 2), pa = lr(ia_, y0 - 2), pid = lr(id_, y0 - 3);
-  CS ps = ZERO ? zs : lr(sig, y0 - 2);
-  for (int b = y0 - 2; b <= y1 + 1; ++b) {
+  CS pu = ZERO ? zs : lr(u, y0 - 1, ob + px), pf = lr(f, y0 - 2, ob), pa = lr(ia_, y0 - 2, ob),
+     pid = lr(id_, y0 - 3, ob - px);
+  CS ps = ZERO ? zs : lr(sig, y0 - 2, ob);
+  // fixed trip count SEG + 4 (rows past y1 load zeros and store nothing); unrolling
+  // (UNR 2-6, renaming the rolling windows) measured no faster than UNR = 1
+  static_assert((SEG + 4) % UNR == 0, "unroll must divide the trip count");
+#pragma unroll UNR
+  for (int it = 0; it < SEG + 4; ++it, ob += px) {
+    const int b = y0 - 2 + it;
     if (!ZERO) {
       ub1 = um1;
       um1 = u0; u0 = up1; up1 = pu;
-      pu = lr(u, b + 2);
+      pu = lr(u, b + 2, ob + 2 * px);
     }
     const CS pf_cur = pf, ps_cur = ps;
     const CD fb = ccast<D, TS>(pf), idb = ccast<D, TS>(pid);
     const CS ab = pa;
-    pf = lr(f, b + 1);
-    pa = lr(ia_, b + 1);
-    pid = lr(id_, b);
-    if (!ZERO) ps = lr(sig, b + 1);
+    pf = lr(f, b + 1, ob + px);
+    pa = lr(ia_, b + 1, ob + px);
+    pid = lr(id_, b, ob);
+    if (!ZERO) ps = lr(sig, b + 1, ob + px);
     // ---- r(b) in TR, t(b).  L u in difference form, sum w (u_nb - u_c): exact
     // algebra because Lc + 4 Lf + 4 Le = 0 (zero ghosts included), and it keeps
     // the cancellation of the compact stencil out of a low-precision sum.
@@ -251,31 +271,33 @@ __global__ void __launch_bounds__(256, 2) k_rb2d_march(Geo g, const cplx<TS> *__
     }
     r2 = r1; r1 = r0; r0 = rb;
     a2 = a1; a1 = a0; a0 = ab;
-    t2 = t1; t1 = t0; t0 = cmul<D>(rb, ccast<D, TS>(ab));
+    {
+      // each row of t and y_c is shuffled once; its left + right sum rolls with the window
+      const CD t0 = cmul<D>(rb, ccast<D, TS>(ab));
+      h2 = h1; h1 = h0; h0 = cadd<D>(shfl_up1(t0), shfl_dn1(t0));
+    }
     // ---- y_c(b-1): diagonal leaves at rows b-2 and b, columns x +- 1
     {
-      const CD sdiag = cadd<D>(cadd<D>(shfl_up1(t2), shfl_dn1(t2)), cadd<D>(shfl_up1(t0), shfl_dn1(t0)));
+      const CD sdiag = cadd<D>(h2, h0);
       const CD num = mkc<D>(r1.x - e * sdiag.x, r1.y - e * sdiag.y);
       const CD yc = in(b - 1) ? cmul<D>(num, idb) : z;
-      c3 = c2; c2 = c1; c1 = yc;
+      c2 = c1; c1 = yc;
+      g3 = g2; g2 = g1; g1 = cadd<D>(shfl_up1(yc), shfl_dn1(yc));
     }
     // ---- output row b-2
     const int yo = b - 2;
     if (yo >= y0 && yo < y1) {
-      const CD cl3 = shfl_up1(c3), cr3 = shfl_dn1(c3), cl1 = shfl_up1(c1), cr1 = shfl_dn1(c1);
       if (out_lane && in(yo)) {
-        // anchors j - (dx, dy) for the 4 diagonal offsets: rows yo -+ 1, columns x -+ 1
-        CD syl = z;
-        int k = 0;
+        // anchors j - (dx, dy) for the 4 diagonal offsets: rows yo -+ 1, columns x -+ 1;
+        // y_c vanishes outside the domain, so the sums need no masking, only the count
+        const CD syl = cadd<D>(g3, g1);
         const bool xm = x - 1 + g.o[0] >= 0, xp = x + 1 + g.o[0] < g.N[0];
         const bool ym = yo - 1 >= ylo, yp = yo + 1 < yhi;
-        if (xm && ym) { syl = cadd<D>(syl, cl3); ++k; }
-        if (xp && ym) { syl = cadd<D>(syl, cr3); ++k; }
-        if (xm && yp) { syl = cadd<D>(syl, cl1); ++k; }
-        if (xp && yp) { syl = cadd<D>(syl, cr1); ++k; }
-        const CD lv = cmul<D>(mkc<D>((D)k * r2.x - e * syl.x, (D)k * r2.y - e * syl.y), ccast<D, TS>(a2));
-        const CD upd = cscale<D>(cadd<D>(c2, lv), w / (D)(1 + k));
-        u_out[col + (int64_t)yo * px] = ccast<TS, D>(ZERO ? upd : cadd<D>(ccast<D, TS>(ub1), upd));
+        const int k = (int)(xm && ym) + (int)(xp && ym) + (int)(xm && yp) + (int)(xp && yp);
+        const D kd = (D)kRbCount[k];
+        const CD lv = cmul<D>(mkc<D>(kd * r2.x - e * syl.x, kd * r2.y - e * syl.y), ccast<D, TS>(a2));
+        const CD upd = cscale<D>(cadd<D>(c2, lv), w * (D)kRbInvCnt[k]);
+        u_out[ob - 2 * px] = ccast<TS, D>(ZERO ? upd : cadd<D>(ccast<D, TS>(ub1), upd));
       }
     }
   }
