@@ -228,7 +228,7 @@ template <typename T> struct Solver : SolverBase {
     int r = 1;      // stored stencil radius
     int rR = 0, rP = 0;
     DBuf coef;      // C [K][total] (levels > 0)
-    DBuf hinv;      // C [k*k][total] (generic patch solve)
+    DBuf bop;       // C [NB][total]: the assembled additive Vanka operator B (Eq. 3.8)
     DBuf u, f, r_, y;
     bool dist = false;          // slab-partitioned (else replicated on every rank)
     int64_t lo = 0, hi = 0;     // this rank's global rows on the slab axis
@@ -379,9 +379,10 @@ template <typename T> struct Solver : SolverBase {
                ih2, Lc, Mc, Le * ih2, rb_ia.template as<C>(), rb_id.template as<C>());
         continue;
       }
-      Lv.hinv.alloc((size_t)k * k * Lv.geo.total * sizeof(C), s);
+      DBuf hv;   // fp64 patch inverses (setup scratch)
+      hv.alloc((size_t)k * k * Lv.geo.total * sizeof(double2), s);
       CK(cudaMemsetAsync(errb.p, 0xff, sizeof(unsigned long long), s));
-      patch_inverse(Lv, cd[l], errb.template as<unsigned long long>(), s);
+      patch_inverse(Lv, cd[l], hv.template as<double2>(), errb.template as<unsigned long long>(), s);
       unsigned long long bad = 0;
       CK(cudaMemcpyAsync(&bad, errb.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -392,9 +393,11 @@ template <typename T> struct Solver : SolverBase {
                  (long long)(bad % nx), (long long)((bad / nx) % ny), (long long)(bad / (nx * ny)));
         throw HmgError(HMG_ESINGULAR_PATCH, buf);
       }
-      // fused levels keep the stored inverses (applied inside the fused sweep):
-      // measured 2.6x faster than factoring 5x5 patches on the fly in fp64
-
+      // assemble B = sum_i V_i^T W_i H_i^{-1} V_i as an NB-point stencil (fp64 sums, stored in T)
+      const int nb = bstencil_planes();
+      Lv.bop.alloc((size_t)nb * Lv.geo.total * sizeof(C), s);
+      assemble_vanka(Lv, hv.template as<double2>(), s);
+      CK(cudaStreamSynchronize(s));
     }
     // coarsest dense inverse (fp64)
     {
@@ -490,7 +493,7 @@ template <typename T> struct Solver : SolverBase {
       gL.total = rowsize(gG) * (gL.n[ax] + 2 * G);
       gL.slab_len = (int64_t)gL.n[ax] * rowsize(gG);
       slice(Lv.coef, sizeof(C), gG, gL, Lv.lo, s);
-      slice(Lv.hinv, sizeof(C), gG, gL, Lv.lo, s);
+      slice(Lv.bop, sizeof(C), gG, gL, Lv.lo, s);
       if (l == 0) {
         slice(sig, sizeof(C), gG, gL, Lv.lo, s);
         slice(sigd, sizeof(D), gG, gL, Lv.lo, s);
@@ -540,12 +543,6 @@ template <typename T> struct Solver : SolverBase {
   // V-cycle residual, whose sigma is fp32)
   bool pair_ok() const { return std::is_same<T, float>::value && opt.dim == 2 && (G % 2) == 0; }
 
-  // Galerkin levels of 2D hierarchies use the fused on-the-fly sweep
-  // (measured: the one-kernel Galerkin sweep k_smooth_stored2d is register- and
-  // phase-bound at ~3.4 TB/s; the two-kernel path -- stored residual at 5.5 TB/s
-  // + direct-gather sweep -- moves 11 % more bytes but streams faster)
-  bool fused_level(int l) const { return false && opt.dim == 2 && l >= 1 && l < L - 1; }
-
   static int kcount(int dim, int r) { return dim == 3 ? (2 * r + 1) * (2 * r + 1) * (2 * r + 1) : (2 * r + 1) * (2 * r + 1); }
 
   void materialize(const Geo &g, double h, const double *pw, const double *pg, DBuf &out, cudaStream_t s) {
@@ -563,27 +560,58 @@ template <typename T> struct Solver : SolverBase {
     }
   }
 
-  void patch_inverse(Level &Lv, DBuf &cd, unsigned long long *err, cudaStream_t s) {
+  int bstencil_planes() const {
+    const int dim = opt.dim;
+    switch (opt.smoother) {
+      case HMG_VANKA_RB: return BStencil<2, PK_RB>::NB;
+      case HMG_VANKA_ELEMENT: return dim == 2 ? BStencil<2, PK_ELEMENT>::NB : BStencil<3, PK_ELEMENT>::NB;
+      case HMG_JACOBI: return dim == 2 ? BStencil<2, PK_JACOBI>::NB : BStencil<3, PK_JACOBI>::NB;
+      case HMG_VANKA_PLUS: return dim == 2 ? BStencil<2, PK_PLUS>::NB : BStencil<3, PK_PLUS>::NB;
+    }
+    throw HmgError(HMG_EINVAL, "unknown smoother");
+  }
+  void assemble_vanka(Level &Lv, const double2 *hv, cudaStream_t s) {
+    auto nl = node_launch(Lv.geo);
+    C *B = Lv.bop.template as<C>();
+    const int dim = opt.dim;
+    switch (opt.smoother) {
+      case HMG_VANKA_RB: launch(k_vanka_assemble<T, 2, PK_RB>, nl.grid, nl.block, 0, s, Lv.geo, hv, B); break;
+      case HMG_VANKA_ELEMENT:
+        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        else launch(k_vanka_assemble<T, 3, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        break;
+      case HMG_JACOBI:
+        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        else launch(k_vanka_assemble<T, 3, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        break;
+      case HMG_VANKA_PLUS:
+        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        else launch(k_vanka_assemble<T, 3, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        break;
+    }
+  }
+
+  // fp64 patch inverses H_i^{-1} into hv [K*K][total] (setup scratch)
+  void patch_inverse(Level &Lv, DBuf &cd, double2 *hv, unsigned long long *err, cudaStream_t s) {
     auto nl = node_launch(Lv.geo);
     const double2 *c = cd.template as<double2>();
-    C *hv = Lv.hinv.template as<C>();
     const int dim = opt.dim;
     switch (opt.smoother) {
       case HMG_VANKA_RB:
         if (dim != 2) throw HmgError(HMG_EINVAL, "RB patch is 2D only (the paper rejects the 13-node 3D RB patch, P:949-951)");
-        launch(k_patch_inverse<T, 2, PK_RB>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        launch(k_patch_inverse<double, 2, PK_RB>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
         break;
       case HMG_VANKA_ELEMENT:
-        if (dim == 2) launch(k_patch_inverse<T, 2, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
-        else launch(k_patch_inverse<T, 3, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        if (dim == 2) launch(k_patch_inverse<double, 2, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        else launch(k_patch_inverse<double, 3, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
         break;
       case HMG_JACOBI:
-        if (dim == 2) launch(k_patch_inverse<T, 2, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
-        else launch(k_patch_inverse<T, 3, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        if (dim == 2) launch(k_patch_inverse<double, 2, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        else launch(k_patch_inverse<double, 3, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
         break;
       case HMG_VANKA_PLUS:
-        if (dim == 2) launch(k_patch_inverse<T, 2, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
-        else launch(k_patch_inverse<T, 3, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        if (dim == 2) launch(k_patch_inverse<double, 2, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
+        else launch(k_patch_inverse<double, 3, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, c, Lv.r, hv, err);
         break;
       default: throw HmgError(HMG_EINVAL, "unknown smoother");
     }
@@ -715,17 +743,16 @@ template <typename T> struct Solver : SolverBase {
     else prolong_t<D>(l, (const D *)e, (const D *)u, (D *)u_out, s);
   }
 
-  // generic Vanka sweep (stored patch inverses, direct gather); TV = level vector type
+  // generic Vanka sweep: the assembled operator B applied as a stencil; TV = level vector type
   template <typename TV, int DIM, int KIND> void vanka_(int l, const void *r, void *u, int zero, cudaStream_t s) {
     Level &Lv = lev[l];
     using BV = decltype(TV{}.x);
     auto nl = node_launch(Lv.geo);
-    constexpr int K = Patch<DIM, KIND>::K;
+    constexpr int NB = BStencil<DIM, KIND>::NB;
     const double nn = (double)Lv.geo.nodes();
-    halo(l, r, 2, s);   // anchors at +-1, their members at +-1 again: r within radius 2
-    tag(zero ? "vanka_direct_zero" : "vanka_direct", l,
-        ((double)K * K * sizeof(C) + (zero ? 2 : 3) * sizeof(TV)) * nn);
-    launch(k_vanka_direct<BV, T, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)Lv.hinv.template as<C>(),
+    halo(l, r, 2, s);   // B reaches offsets up to +-2 (RB / Plus)
+    tag(zero ? "vanka_zero" : "vanka", l, ((double)NB * sizeof(C) + (zero ? 2 : 3) * sizeof(TV)) * nn);
+    launch(k_vanka_stencil<BV, T, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)Lv.bop.template as<C>(),
            (const TV *)r, (const TV *)u, (TV *)u, (BV)damp(l), zero);
   }
   template <typename TV> void vanka_kind(int l, const void *r, void *u, int zero, cudaStream_t s) {
@@ -740,7 +767,7 @@ template <typename T> struct Solver : SolverBase {
 
   // Do the level's sweeps read neighbours of u inside one kernel?  Then they
   // must run out of place (other blocks may still read the old u).
-  bool fused_sweep(int l) const { return (l == 0 && rb_closed) || fused_level(l); }
+  bool fused_sweep(int l) const { return l == 0 && rb_closed; }
 
   // one additive Vanka relaxation (Eq. 3.8): u_out = u + w B (f - A u);
   // zero: u == 0 (u may be null).  Fused levels: u_out != u required;
@@ -776,19 +803,6 @@ template <typename T> struct Solver : SolverBase {
         if (c4) launch(k_rb2d_march<T, ST_COMPACT4, false, SEG, double, T, 1, MB>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
         else launch(k_rb2d_march<T, ST_FD2, false, SEG, double, T, 1, MB>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
       }
-      return;
-    }
-    if (fused_level(l)) {
-      const int K = patch_size(opt.dim, opt.smoother);
-      const double planes = zero ? (K > 1 ? 13.0 : 1.0) : (double)kcount(opt.dim, Lv.r);
-      if (!zero) halo(l, u, 2 + Lv.r, s);
-      halo(l, f, 2, s);
-      const double hplanes = Lv.hinv.p ? (double)K * K : 0.0;
-      tag(zero ? "smooth_stored_zero" : "smooth_stored", l,
-          ((Lv.hinv.p ? (zero ? 0.0 : kcount(opt.dim, Lv.r)) : planes) + hplanes) * sizeof(C) * nn +
-              (zero ? 2 : 3) * sizeof(D) * nn);
-      smooth_stored2d<T>(Lv.r, opt.smoother, zero != 0, Lv.geo, (const C *)Lv.coef.template as<C>(),
-                         (const C *)Lv.hinv.template as<C>(), (const D *)f, (const D *)u, (D *)u_out, w, s);
       return;
     }
     if (u_out != u && !zero) CK(cudaMemcpyAsync(u_out, u, Lv.geo.total * vsize(l), cudaMemcpyDeviceToDevice, s));

@@ -252,6 +252,37 @@ __global__ void k_patch_inverse(Geo g, const double2 *__restrict__ coef, int r, 
       hinv[(int64_t)(mem[a] * K + mem[b]) * g.total + c] = ok ? ccast<T, double>(X[a][b]) : mkc<T>(0, 0);
 }
 
+// Assemble the additive Vanka operator B (k_vanka.cuh, BStencil) from the fp64
+// patch inverses: B[d][j] = (1/cnt_j) sum_{s,q: o_q - o_s = d} Hinv_{j - o_s}[s][q]
+// (Eq. 3.8; non-anchor positions hold zero inverses).  fp64 sums, stored in T.
+template <typename T, int DIM, int KIND>
+__global__ void k_vanka_assemble(Geo g, const double2 *__restrict__ hinv, cplx<T> *__restrict__ B) {
+  HMG_NODE_IDX(g, ix, iy, iz);
+  using P = Patch<DIM, KIND>;
+  using S = BStencil<DIM, KIND>;
+  constexpr int K = P::K;
+  const int64_t j = g.idx(ix, iy, iz);
+  const double ic = 1.0 / (double)P::count(g, ix, iy, iz);
+  static_for<0, S::NB>([&](auto PI) {
+    constexpr int p = decltype(PI)::value;
+    double2 acc = make_double2(0, 0);
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        int ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+        P::off(a, ax, ay, az);
+        P::off(b, bx, by, bz);
+        if (bx - ax != S::template dx<p> || by - ay != S::template dy<p> || bz - az != S::template dz<p>) continue;
+        const double2 h = hinv[(int64_t)(a * K + b) * g.total + g.idx(ix - ax, iy - ay, iz - az)];
+        acc.x += h.x;
+        acc.y += h.y;
+      }
+    }
+    B[(int64_t)p * g.total + j] = mkc<T>((T)(acc.x * ic), (T)(acc.y * ic));
+  });
+}
+
 // a8: dense coarsest matrix (row-major, compact x-fastest indices)
 static __global__ void k_dense_assemble(Geo g, const double2 *__restrict__ coef, int r, double2 *__restrict__ A) {
   HMG_NODE_IDX(g, ix, iy, iz);

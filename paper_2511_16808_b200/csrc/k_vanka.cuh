@@ -13,6 +13,8 @@
 // y_c = H_c^{-1} r[X_c] that belongs to j, and applies w/cnt_j (the weight
 // depends on j only, so it factors out).  No atomics, deterministic order.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "k_operator.cuh"
 
@@ -22,7 +24,7 @@ enum { PK_RB = 0, PK_ELEMENT = 1, PK_JACOBI = 2, PK_PLUS = 3 };
 
 template <int DIM, int KIND> struct Patch {
   static constexpr int K = KIND == PK_JACOBI ? 1 : KIND == PK_ELEMENT ? (1 << DIM) : KIND == PK_PLUS ? 2 * DIM + 1 : 5;
-  __host__ __device__ static __forceinline__ void off(int s, int &ox, int &oy, int &oz) {
+  __host__ __device__ static constexpr void off(int s, int &ox, int &oy, int &oz) {
     ox = oy = oz = 0;
     if (KIND == PK_JACOBI) return;
     if (KIND == PK_ELEMENT) { ox = s & 1; oy = (s >> 1) & 1; oz = (s >> 2) & 1; return; }
@@ -68,42 +70,82 @@ template <int DIM, int KIND> struct Patch {
 // 1 / cnt_j for cnt_j = 1..8 (a table instead of a per-node fp64 division)
 __constant__ double kInvCount[9] = {0.0, 1.0, 0.5, 1.0 / 3.0, 0.25, 0.2, 1.0 / 6.0, 1.0 / 7.0, 0.125};
 
-// (1a) generic sweep with stored inverses, as a direct gather (any dim/kind):
-//   u_out_j = u_j + (w/cnt_j) sum_{s: anchor c = j - o_s} sum_q Hinv_c[s][q] r[c + o_q]
-// (r = f - A u precomputed; r = f for a zero initial guess).  Only row s of
-// each containing anchor's inverse is read, so every stored entry is read once
-// per sweep and no patch solution is staged.  Each node reads/writes only its
-// own u: in place is safe.  Branch-free: a position c = j - o_s that is not an
-// anchor (outside the domain, or an Element corner on the far faces) holds an
-// all-zero inverse (buffers are zeroed at allocation, k_patch_inverse writes
-// anchors only; slab ghost rows hold the neighbour's anchors), and r is finite
-// there (zero ghosts / exchanged halo), so its terms vanish exactly and every
-// load of the node can be in flight at once.
-template <typename T, typename TK, int DIM, int KIND>
-__global__ void __launch_bounds__(256) k_vanka_direct(Geo g, const cplx<TK> *__restrict__ hinv,
-                                                      const cplx<T> *__restrict__ r, const cplx<T> *u,
-                                                      cplx<T> *u_out, T w, int zero) {
-  HMG_NODE_IDX(g, ix, iy, iz);
-  using P = Patch<DIM, KIND>;
-  constexpr int K = P::K;
-  cplx<T> acc = mkc<T>(0, 0);
-#pragma unroll
-  for (int sI = 0; sI < K; ++sI) {
-    int dx, dy, dz;
-    P::off(sI, dx, dy, dz);
-    const int64_t c = g.idx(ix - dx, iy - dy, iz - dz);
-    cplx<TK> hw[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) hw[q] = hinv[(int64_t)(sI * K + q) * g.total + c];
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      int bx, by, bz;
-      P::off(q, bx, by, bz);
-      acc = cfma<T>(acc, ccast<T, TK>(hw[q]), r[c + g.delta(bx, by, bz)]);
-    }
+// (1a) the additive Vanka operator ASSEMBLED as a stencil.
+//   B = sum_i V_i^T W_i H_i^{-1} V_i   (Eq. 3.8; W_i(j,j) = 1/cnt_j)
+// couples node j only to j + d with d = o_q - o_s for two offsets o_s, o_q of the
+// patch shape, so B is a short stencil: 13 offsets for RB / Plus 2D, 9 (27) for
+// Element 2D (3D), 25 for Plus 3D, 1 for Jacobi -- against K^2 = 25 (64) inverse
+// entries a per-node gather over the containing patches reads.  B is assembled
+// once at setup in fp64 from the fp64 patch inverses (k_vanka_assemble) and
+// stored in the level's coefficient precision; a sweep is then
+//   u_out = u + w B r   (r = f - A u, or r = f for a zero initial guess).
+// Mathematically the same operator (only the summation order differs).
+template <int DIM, int KIND> struct BStencil {
+  static constexpr int K = Patch<DIM, KIND>::K;
+  struct Tab {
+    int n = 0;
+    int d[64][3] = {};
+  };
+  static constexpr Tab make() {
+    Tab t;
+    const int zr = DIM == 3 ? 2 : 0;
+    for (int dz = -zr; dz <= zr; ++dz)
+      for (int dy = -2; dy <= 2; ++dy)
+        for (int dx = -2; dx <= 2; ++dx) {
+          bool hit = false;
+          for (int a = 0; a < K; ++a)
+            for (int b = 0; b < K; ++b) {
+              int ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+              Patch<DIM, KIND>::off(a, ax, ay, az);
+              Patch<DIM, KIND>::off(b, bx, by, bz);
+              if (bx - ax == dx && by - ay == dy && bz - az == dz) hit = true;
+            }
+          if (hit) {
+            t.d[t.n][0] = dx;
+            t.d[t.n][1] = dy;
+            t.d[t.n][2] = dz;
+            ++t.n;
+          }
+        }
+    return t;
   }
+  static constexpr Tab tab = make();
+  static constexpr int NB = tab.n;
+  template <int P> static constexpr int dx = tab.d[P][0];
+  template <int P> static constexpr int dy = tab.d[P][1];
+  template <int P> static constexpr int dz = tab.d[P][2];
+};
+
+static_assert(BStencil<2, PK_RB>::NB == 13 && BStencil<2, PK_PLUS>::NB == 13 && BStencil<3, PK_PLUS>::NB == 25,
+              "RB / Plus operator offsets");
+static_assert(BStencil<2, PK_ELEMENT>::NB == 9 && BStencil<3, PK_ELEMENT>::NB == 27 && BStencil<2, PK_JACOBI>::NB == 1,
+              "Element / Jacobi operator offsets");
+
+template <int I, int N, typename F>
+__device__ __forceinline__ void static_for(F &&f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(f);
+  }
+}
+
+// u_out_j = u_j + w sum_p B[p][j] r[j + d_p]   (u unused when zero; in place is safe:
+// every node reads and writes only its own u).  B vanishes at non-anchor /
+// out-of-domain positions and r is zero (ghosts) or exchanged (halo) there.
+template <typename T, typename TK, int DIM, int KIND>
+__global__ void __launch_bounds__(256) k_vanka_stencil(Geo g, const cplx<TK> *__restrict__ B,
+                                                       const cplx<T> *__restrict__ r, const cplx<T> *u,
+                                                       cplx<T> *u_out, T w, int zero) {
+  HMG_NODE_IDX(g, ix, iy, iz);
+  using S = BStencil<DIM, KIND>;
   const int64_t j = g.idx(ix, iy, iz);
-  const cplx<T> upd = cscale<T>(acc, w * (T)kInvCount[P::count(g, ix, iy, iz)]);
+  cplx<T> acc = mkc<T>(0, 0);
+  static_for<0, S::NB>([&](auto P) {
+    constexpr int p = decltype(P)::value;
+    const cplx<T> b = ccast<T, TK>(B[(int64_t)p * g.total + j]);
+    acc = cfma<T>(acc, b, r[j + g.delta(S::template dx<p>, S::template dy<p>, S::template dz<p>)]);
+  });
+  const cplx<T> upd = cscale<T>(acc, w);
   u_out[j] = zero ? upd : cadd<T>(u[j], upd);
 }
 
@@ -299,153 +341,6 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
         const CD upd = cscale<D>(cadd<D>(c2, lv), w * (D)kRbInvCnt[k]);
         u_out[ob - 2 * px] = ccast<TS, D>(ZERO ? upd : cadd<D>(ccast<D, TS>(ub1), upd));
       }
-    }
-  }
-}
-
-// Dense K x K complex solve A y = b in registers, Gaussian elimination with
-// partial pivoting (row swaps by static-index selects, so A stays in
-// registers); same pivoting rule as LAPACK getrf.  b is overwritten by y.
-template <typename T, int K>
-__device__ __forceinline__ void small_solve(cplx<T> (&A)[K][K], cplx<T> (&b)[K]) {
-  cplx<T> ipiv[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    T best = cabs2<T>(A[k][k]);
-    int p = k;
-#pragma unroll
-    for (int i = k + 1; i < K; ++i) {
-      const T v = cabs2<T>(A[i][k]);
-      if (v > best) { best = v; p = i; }
-    }
-#pragma unroll
-    for (int i = k + 1; i < K; ++i) {
-      const bool sw = i == p;   // branch-free select keeps A in registers
-#pragma unroll
-      for (int c = k; c < K; ++c) {
-        const cplx<T> t = A[k][c];
-        A[k][c] = cselp<T>(sw, A[i][c], t);
-        A[i][c] = cselp<T>(sw, t, A[i][c]);
-      }
-      const cplx<T> t = b[k];
-      b[k] = cselp<T>(sw, b[i], t);
-      b[i] = cselp<T>(sw, t, b[i]);
-    }
-    ipiv[k] = crecip_fast<T>(A[k][k]);
-#pragma unroll
-    for (int i = k + 1; i < K; ++i) {
-      const cplx<T> f = cmul<T>(A[i][k], ipiv[k]);
-#pragma unroll
-      for (int c = k + 1; c < K; ++c) A[i][c] = csub<T>(A[i][c], cmul<T>(f, A[k][c]));
-      b[i] = csub<T>(b[i], cmul<T>(f, b[k]));
-    }
-  }
-#pragma unroll
-  for (int k = K - 1; k >= 0; --k) {
-    cplx<T> acc = b[k];
-#pragma unroll
-    for (int c = k + 1; c < K; ++c) acc = csub<T>(acc, cmul<T>(A[k][c], b[c]));
-    b[k] = cmul<T>(acc, ipiv[k]);
-  }
-}
-
-// (1c) one additive-Vanka sweep on a Galerkin level in ONE kernel (2D,
-// stored stencil of radius R): residual on the tile + 2 into shared memory,
-// then every output node j gathers its patch values DIRECTLY,
-//     u_j += w/cnt_j sum_{s: anchor c = j - o_s} sum_b Hinv_c[s][b] r[c + o_b],
-// i.e. only row s of each containing anchor's inverse is needed; every
-// stored inverse entry is still read exactly once per sweep and no patch
-// solution is staged (reading A8: H_i = A_l[X_i, X_i], inverses formed at
-// setup in fp64 by k_patch_inverse).  HBM: stencil planes (residual), inverse
-// planes, u, f read once, u' written once (ZERO: inverse planes and f only).
-// Out of place (u_out != u): other blocks still read old u in their halos.
-// Without stored inverses (hinv == nullptr) each anchor's patch matrix is
-// assembled from the stencil and solved in registers (k_smooth_stored2d_lu).
-template <typename T, typename TK, int R, int KIND, int TX, int TY, bool ZERO>
-__global__ void __launch_bounds__(256) k_smooth_stored2d(Geo g, const cplx<TK> *__restrict__ coef,
-                                                         const cplx<TK> *__restrict__ hinv,
-                                                         const cplx<T> *__restrict__ f, const cplx<T> *__restrict__ u,
-                                                         cplx<T> *__restrict__ u_out, T w) {
-  using P = Patch<2, KIND>;
-  constexpr int K = P::K;
-  constexpr int NT = 256;
-  constexpr int WS = 2 * R + 1;
-  constexpr int HU = 2 + R;
-  constexpr int UX = TX + 2 * HU, UY = TY + 2 * HU, RX = TX + 4, RY = TY + 4;
-  constexpr int NU = (UX * UY + NT - 1) / NT, NR = (RX * RY + NT - 1) / NT;
-  __shared__ cplx<T> su[ZERO ? 1 : UY * UX];
-  __shared__ cplx<T> sr[RY * RX];
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  const cplx<T> zero = mkc<T>(0, 0);
-  if (!ZERO) {
-#pragma unroll
-    for (int k = 0; k < NU; ++k) {
-      const int i = tid + k * NT;
-      if (i < UY * UX) {
-        const int gx = x0 - HU + i % UX, gy = y0 - HU + i / UX;
-        su[i] = g.inside(gx, gy, 0) ? u[g.idx(gx, gy, 0)] : zero;
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NR; ++k) {
-    const int i = tid + k * NT;
-    if (i < RY * RX) {
-      const int gx = x0 - 2 + i % RX, gy = y0 - 2 + i / RX;
-      sr[i] = g.inside(gx, gy, 0) ? f[g.idx(gx, gy, 0)] : zero;
-    }
-  }
-  __syncthreads();
-  if (!ZERO) {
-#pragma unroll
-    for (int k = 0; k < NR; ++k) {
-      const int i = tid + k * NT;
-      if (i >= RY * RX) continue;
-      const int lx = i % RX, ly = i / RX;
-      const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
-      if (!g.inside(gx, gy, 0)) continue;
-      const int64_t j = g.idx(gx, gy, 0);
-      const cplx<T> *uc = su + (ly + R) * UX + (lx + R);
-      cplx<T> acc = zero;
-#pragma unroll
-      for (int oy = -R; oy <= R; ++oy) {
-        cplx<TK> cw[WS];
-#pragma unroll
-        for (int ox = -R; ox <= R; ++ox) cw[ox + R] = coef[(int64_t)((ox + R) + WS * (oy + R)) * g.total + j];
-#pragma unroll
-        for (int ox = -R; ox <= R; ++ox) acc = cfma<T>(acc, ccast<T, TK>(cw[ox + R]), uc[oy * UX + ox]);
-      }
-      sr[i] = csub<T>(sr[i], acc);
-    }
-    __syncthreads();
-  }
-  for (int oy = threadIdx.y; oy < TY; oy += blockDim.y) {
-    for (int ox = threadIdx.x; ox < TX; ox += blockDim.x) {
-      const int gx = x0 + ox, gy = y0 + oy;
-      if (!g.inside(gx, gy, 0)) continue;
-      cplx<T> acc = zero;
-#pragma unroll
-      for (int sI = 0; sI < K; ++sI) {
-        int dx, dy, dz;
-        P::off(sI, dx, dy, dz);
-        const int cx = gx - dx, cy = gy - dy;   // anchor whose patch holds j in slot sI
-        if (!P::anchor(g, cx, cy, 0)) continue;
-        const int64_t c = g.idx(cx, cy, 0);
-        cplx<TK> hw[K];
-#pragma unroll
-        for (int q = 0; q < K; ++q) hw[q] = hinv[(int64_t)(sI * K + q) * g.total + c];
-#pragma unroll
-        for (int q = 0; q < K; ++q) {
-          int bx, by, bz;
-          P::off(q, bx, by, bz);
-          // members outside the domain have zero inverse columns and r = 0 there
-          acc = cfma<T>(acc, ccast<T, TK>(hw[q]), sr[(oy + 2 - dy + by) * RX + (ox + 2 - dx + bx)]);
-        }
-      }
-      const cplx<T> upd = cscale<T>(acc, w / (T)P::count(g, gx, gy, 0));
-      const int64_t j = g.idx(gx, gy, 0);
-      u_out[j] = ZERO ? upd : cadd<T>(su[(oy + HU) * UX + (ox + HU)], upd);
     }
   }
 }

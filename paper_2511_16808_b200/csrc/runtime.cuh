@@ -83,11 +83,4 @@ template <>
 int krylov_axpy<float, float>(int nv, const float2 *V, int64_t vstride, const double2 *coef, const double *vscale,
                               double sgn, float2 *w, int64_t len, double2 *partial_norm, cudaStream_t s);
 
-// Fused Galerkin-level Vanka sweep, 2D (smooth2d.cu).
-// hinv == nullptr: patches factored on the fly in every sweep; else the
-// stored patch inverses are applied.
-template <typename T>
-void smooth_stored2d(int r, int kind, bool zero, const Geo &g, const cplx<T> *coef, const cplx<T> *hinv,
-                     const double2 *f, const double2 *u, double2 *u_out, double w, cudaStream_t s);
-
 }  // namespace hmg
