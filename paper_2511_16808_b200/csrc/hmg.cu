@@ -794,14 +794,21 @@ template <typename T> struct Solver : SolverBase {
       // all arithmetic in fp64 (fp32 patch algebra -- with or
       // without an fp64 residual, in the post-sweep alone -- moved config 0 from
       // 30 to 34 iterations on the B200 while saving ~10 % at N = 4096)
+      // rows stream through a cp.async ring PD = 2 rows ahead (measured: PD 1 / 3 slower)
+      constexpr int PD = 2;
+      auto go = [&](auto kern, int na) {
+        const int smem = 8 * (PD + 2) * na * 32 * (int)sizeof(C);
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        launch(kern, grid, block, (size_t)smem, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+      };
+      // c64 non-zero: 3 blocks/SM (80 registers) measured 16 % faster than 2 (91 registers)
+      constexpr int MB = sizeof(T) == 4 ? 3 : 2;
       if (zero) {
-        if (c4) launch(k_rb2d_march<T, ST_COMPACT4, true, SEG, double, double>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
-        else launch(k_rb2d_march<T, ST_FD2, true, SEG, double, double>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        if (c4) go(k_rb2d_march<T, ST_COMPACT4, true, SEG, double, double, 1, 2, PD>, 3);
+        else go(k_rb2d_march<T, ST_FD2, true, SEG, double, double, 1, 2, PD>, 3);
       } else {
-        // c64: 3 blocks/SM (80 registers, 24 B spill) measured 16 % faster than 2 (91 registers)
-        constexpr int MB = sizeof(T) == 4 ? 3 : 2;
-        if (c4) launch(k_rb2d_march<T, ST_COMPACT4, false, SEG, double, T, 1, MB>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
-        else launch(k_rb2d_march<T, ST_FD2, false, SEG, double, T, 1, MB>, grid, block, 0, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        if (c4) go(k_rb2d_march<T, ST_COMPACT4, false, SEG, double, T, 1, MB, PD>, 5);
+        else go(k_rb2d_march<T, ST_FD2, false, SEG, double, T, 1, MB, PD>, 5);
       }
       return;
     }

@@ -215,7 +215,7 @@ __constant__ double kRbInvCnt[5] = {1.0, 0.5, 1.0 / 3.0, 0.25, 0.2};
 // TC = arithmetic precision of the patch algebra (fp64, or the storage
 // precision), TR = precision of the residual f - H_s u
 template <typename TS, int KIND, bool ZERO, int SEG, typename TC = double, typename TR = double, int UNR = 1,
-          int MINB = 2>
+          int MINB = 2, int PD = 1>
 __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> *__restrict__ sig,
                                                     const cplx<TS> *__restrict__ ia_, const cplx<TS> *__restrict__ id_,
                                                     double alpha_d, double ih2_d, const cplx<TS> *__restrict__ f,
@@ -262,27 +262,54 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
     u0 = lr(u, y0 - 3, ob - px);
     up1 = lr(u, y0 - 2, ob);
   }
-  CS pu = ZERO ? zs : lr(u, y0 - 1, ob + px), pf = lr(f, y0 - 2, ob), pa = lr(ia_, y0 - 2, ob),
-     pid = lr(id_, y0 - 3, ob - px);
-  CS ps = ZERO ? zs : lr(sig, y0 - 2, ob);
+  // Row streaming through a per-warp shared-memory ring filled by cp.async (zero
+  // fill for rows outside the domain), PD rows ahead.  Each lane copies and reads
+  // only its own column, so no barrier is needed.  (Register prefetch measured
+  // slower: the compiler moves each just-issued load into the loop-carried
+  // register at the back edge, and that move waits for the load.)
+  constexpr int NA = ZERO ? 3 : 5;   // f, ia, id (+ u, sigma)
+  constexpr int NST = PD + 2;
+  extern __shared__ __align__(16) unsigned char rb_smem[];
+  CS *ring = reinterpret_cast<CS *>(rb_smem) + (size_t)(threadIdx.x >> 5) * (NST * NA * 32);
+  const int64_t ob0 = ob;
+  auto cp = [&](const CS *a, int y, int64_t o, int slot, int k) {
+    const bool ok = in(y);
+    const CS *gp = ok ? a + o : a;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(ring + (slot * NA + k) * 32 + lane);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(sa), "l"(gp), "n"((int)sizeof(CS)),
+                 "r"(ok ? (int)sizeof(CS) : 0)
+                 : "memory");
+  };
+  auto issue = [&](int it_) {   // the rows step it_ consumes
+    const int b_ = y0 - 2 + it_, slot = it_ % NST;
+    const int64_t o = ob0 + (int64_t)it_ * px;
+    cp(f, b_, o, slot, 0);
+    cp(ia_, b_, o, slot, 1);
+    cp(id_, b_ - 1, o - px, slot, 2);
+    if (!ZERO) {
+      cp(u, b_ + 1, o + px, slot, 3);
+      cp(sig, b_, o, slot, 4);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int k = 0; k < PD; ++k) issue(k);
   // fixed trip count SEG + 4 (rows past y1 load zeros and store nothing); unrolling
   // (UNR 2-6, renaming the rolling windows) measured no faster than UNR = 1
   static_assert((SEG + 4) % UNR == 0, "unroll must divide the trip count");
 #pragma unroll UNR
   for (int it = 0; it < SEG + 4; ++it, ob += px) {
     const int b = y0 - 2 + it;
+    issue(it + PD);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(PD) : "memory");
+    const CS *sl = ring + (it % NST) * NA * 32 + lane;
     if (!ZERO) {
       ub1 = um1;
-      um1 = u0; u0 = up1; up1 = pu;
-      pu = lr(u, b + 2, ob + 2 * px);
+      um1 = u0; u0 = up1; up1 = sl[3 * 32];
     }
-    const CS pf_cur = pf, ps_cur = ps;
-    const CD fb = ccast<D, TS>(pf), idb = ccast<D, TS>(pid);
-    const CS ab = pa;
-    pf = lr(f, b + 1, ob + px);
-    pa = lr(ia_, b + 1, ob + px);
-    pid = lr(id_, b, ob);
-    if (!ZERO) ps = lr(sig, b + 1, ob + px);
+    const CS pf_cur = sl[0], ps_cur = ZERO ? zs : sl[4 * 32];
+    const CD fb = ccast<D, TS>(pf_cur), idb = ccast<D, TS>(sl[2 * 32]);
+    const CS ab = sl[32];
     // ---- r(b) in TR, t(b).  L u in difference form, sum w (u_nb - u_c): exact
     // algebra because Lc + 4 Lf + 4 Le = 0 (zero ghosts included), and it keeps
     // the cancellation of the compact stencil out of a low-precision sum.
