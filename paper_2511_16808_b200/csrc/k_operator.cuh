@@ -42,14 +42,14 @@ template <> struct FineW<3, ST_FD2> {
 // sig[j] = sigma_j = (w^2k^2, -w^2k^2 g/w); alpha = shift (0 for H).
 // TC = arithmetic precision (T or double); storage of x, f, y stays T;
 // TS = storage precision of sigma.
-template <typename T, int DIM, int KIND, typename TC = T, typename TS = T>
-__global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<TS> *__restrict__ sig, TC alpha, TC ih2,
-                                                 const cplx<T> *__restrict__ x,
-                                                 const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y) {
-  HMG_NODE_IDX(g, ix, iy, iz);
+// (A x)_i or (f - A x)_i at padded index i, rounded to T (shared by every kernel
+// that forms the fine operator, so their results agree bit for bit)
+template <typename T, int DIM, int KIND, typename TC, typename TS>
+__device__ __forceinline__ cplx<T> fine_op_node(const Geo &g, const cplx<TS> *__restrict__ sig, TC alpha, TC ih2,
+                                                const cplx<T> *__restrict__ x, const cplx<T> *__restrict__ f,
+                                                int64_t i) {
   using W = FineW<DIM, KIND>;
   using CC = cplx<TC>;
-  const int64_t i = g.idx(ix, iy, iz);
   const int64_t px = g.px;
   auto X = [&](int64_t k) { return ccast<TC, T>(x[k]); };
   const CC xc = X(i);
@@ -77,7 +77,16 @@ __global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<TS> *__restri
   CC s = ccast<TC, TS>(sig[i]);
   s.y = fma(-alpha, s.x, s.y);
   const CC Ax = csub<TC>(Lx, cmul<TC>(s, Mx));
-  y[i] = ccast<T, TC>(f ? csub<TC>(ccast<TC, T>(f[i]), Ax) : Ax);
+  return ccast<T, TC>(f ? csub<TC>(ccast<TC, T>(f[i]), Ax) : Ax);
+}
+
+template <typename T, int DIM, int KIND, typename TC = T, typename TS = T>
+__global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<TS> *__restrict__ sig, TC alpha, TC ih2,
+                                                 const cplx<T> *__restrict__ x,
+                                                 const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y) {
+  HMG_NODE_IDX(g, ix, iy, iz);
+  const int64_t i = g.idx(ix, iy, iz);
+  y[i] = fine_op_node<T, DIM, KIND, TC, TS>(g, sig, alpha, ih2, x, f, i);
 }
 
 // 2D c64 variant of k_fine_op: one thread per PAIR of x-adjacent nodes
