@@ -207,6 +207,23 @@ HMG_API hmg_status hmg_fgmres_solve_host(const hmg_hierarchy *hier, const void *
                                  int restart, double tol, int maxiter, void *stream,
                                  hmg_report *rep);
 
+/* Multi-RHS batch (the paper's use case of many sources on
+ * one medium): nrhs independent FGMRES(restart) solves H x_k = q_k
+ * on the same hierarchy, advanced in lockstep.  Each step applies ONE batched
+ * preconditioner: the fine level runs per right-hand side, every coarser level
+ * once for the whole batch, so each stored stencil / Vanka-operator coefficient
+ * and the coarsest inverse are read once per step for all right-hand sides.
+ * Per right-hand side the arithmetic is that of hmg_fgmres_solve (identical
+ * iterates and iteration counts).
+ *   q, x : device arrays of nrhs * N complex values (N = fine node count),
+ *          right-hand side k at offset k * N; caller-owned.
+ *   reps : NULL or an array of nrhs reports (seconds = the whole batch).
+ * One rank only (HMG_EINVAL on a slab-partitioned hierarchy).  Returns HMG_OK,
+ * or HMG_ENOTCONVERGED if any right-hand side missed tol within maxiter. */
+HMG_API hmg_status hmg_fgmres_solve_batch(const hmg_hierarchy *hier, int nrhs, const void *q, void *x,
+                                          int restart, double tol, int maxiter, void *stream,
+                                          hmg_report *reps);
+
 /* Introspection. */
 HMG_API int hmg_num_levels(const hmg_hierarchy *hier);
 HMG_API int64_t hmg_level_nodes(const hmg_hierarchy *hier, int level, int64_t nodes_per_axis[3]);

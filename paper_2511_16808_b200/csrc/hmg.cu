@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -143,25 +144,36 @@ __global__ void k_identity(int N, double2 *__restrict__ A) {
   if (i < (int64_t)N * N) A[i] = make_double2((i / N) == (i % N) ? 1.0 : 0.0, 0.0);
 }
 
-template <typename T> __global__ void k_coarse_gemv(Geo g, const double2 *__restrict__ Ainv,
-                                                    const cplx<T> *__restrict__ r, cplx<T> *__restrict__ e) {
+// e = A_L^{-1} r for nr right-hand sides at a stride of bs (one warp per row; each
+// row of the inverse is read once for all of them)
+template <typename T, int NR = 1>
+__global__ void k_coarse_gemv(Geo g, const double2 *__restrict__ Ainv, const cplx<T> *__restrict__ r,
+                              cplx<T> *__restrict__ e, int64_t bs = 0) {
   const int N = (int)g.nodes();
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= N) return;
-  double ax = 0, ay = 0;
+  double ax[NR], ay[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) ax[q] = ay[q] = 0;
   for (int col = lane; col < N; col += 32) {
     const int cx = col % g.n[0], cy = (col / g.n[0]) % g.n[1], cz = col / (g.n[0] * g.n[1]);
-    const cplx<T> v = r[g.idx(cx, cy, cz)];
+    const int64_t ci = g.idx(cx, cy, cz);
     const double2 a = Ainv[(int64_t)row * N + col];
-    ax = fma(a.x, (double)v.x, fma(-a.y, (double)v.y, ax));
-    ay = fma(a.x, (double)v.y, fma(a.y, (double)v.x, ay));
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const cplx<T> v = r[q * bs + ci];
+      ax[q] = fma(a.x, (double)v.x, fma(-a.y, (double)v.y, ax[q]));
+      ay[q] = fma(a.x, (double)v.y, fma(a.y, (double)v.x, ay[q]));
+    }
   }
-  ax = warp_sum(ax);
-  ay = warp_sum(ay);
-  if (lane == 0) {
-    const int rx = row % g.n[0], ry = (row / g.n[0]) % g.n[1], rz = row / (g.n[0] * g.n[1]);
-    e[g.idx(rx, ry, rz)] = mkc<T>((T)ax, (T)ay);
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const double sx = warp_sum(ax[q]), sy = warp_sum(ay[q]);
+    if (lane == 0) {
+      const int rx = row % g.n[0], ry = (row / g.n[0]) % g.n[1], rz = row / (g.n[0] * g.n[1]);
+      e[q * bs + g.idx(rx, ry, rz)] = mkc<T>((T)sx, (T)sy);
+    }
   }
 }
 
@@ -181,6 +193,8 @@ struct SolverBase {
   virtual void api_vcycle(const void *f, void *x, int zero, cudaStream_t s) = 0;
   virtual hmg_status api_fgmres(const void *q, void *x, int host, int restart, double tol, int maxiter,
                                 cudaStream_t s, hmg_report *rep) = 0;
+  virtual hmg_status api_fgmres_batch(int nrhs, const void *q, void *x, int host, int restart, double tol,
+                                      int maxiter, cudaStream_t s, hmg_report *reps) = 0;
   virtual int64_t level_nodes(int level, int64_t n[3]) const = 0;
   virtual int radius(int level) const = 0;
   virtual int copy_stencil(int level, double *out, int64_t cap) = 0;
@@ -251,16 +265,19 @@ template <typename T> struct Solver : SolverBase {
   int reorth = 0;         // second Gram-Schmidt passes in the last solve
   // CUDA graph of the coarse part of the cycle (levels >= 1 run on fixed
   // buffers, so one capture serves every call); single-rank runs only
-  cudaGraphExec_t cgraph = nullptr;
+  std::map<int, cudaGraphExec_t> cgraphs;   // coarse-cycle graph per batch width
+  std::map<int, long long> cgraph_kernels_nr;
+  // multi-RHS batches: levels >= 1 hold nrb right-hand sides at a stride of one
+  // padded box (capacity nrb_cap); the fine level runs per right-hand side
+  int nrb = 1, nrb_cap = 1;
   cudaStream_t gstream = nullptr;
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
-  long long cgraph_kernels = 0;
   int nblk = 0;
   double *hpin = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   ~Solver() override {
-    if (cgraph) cudaGraphExecDestroy(cgraph);
+    for (auto &kv : cgraphs) cudaGraphExecDestroy(kv.second);
     if (gev_in) cudaEventDestroy(gev_in);
     if (gev_out) cudaEventDestroy(gev_out);
     if (gstream) cudaStreamDestroy(gstream);
@@ -531,7 +548,7 @@ template <typename T> struct Solver : SolverBase {
   // Slabs: the coarse slab's R P support, fine rows [2 lo - rR - 1, 2 (hi - 1) + rR + 1],
   // must lie inside the fine slab's ghosted rows (sigma is sliced with G ghost rows).
   bool mf_level1(int l) const {
-    if (l != 1 || L < 2 || opt.dim != 2 || opt.coarse_op != HMG_GALERKIN || !std::getenv("HMG_MF1")) return false;
+    if (l != 1 || L < 2 || nrb != 1 || opt.dim != 2 || opt.coarse_op != HMG_GALERKIN || !std::getenv("HMG_MF1")) return false;
     const Level &F = lev[0], &C1 = lev[1];
     if (!F.dist) return true;
     if (!C1.dist) return false;
@@ -625,6 +642,20 @@ template <typename T> struct Solver : SolverBase {
   static constexpr size_t vsize(int l) { return l == 0 ? sizeof(C) : sizeof(D); }
 
   // y = A_l x  or  y = f - A_l x
+  // batch width at level l (the fine level always runs one right-hand side per call)
+  int nbat(int l) const { return l == 0 ? 1 : nrb; }
+  // fn(std::integral_constant<int, NR>, q0) over chunks (8, 4, 2, 1) of n right-hand sides
+  template <typename Fn> static void over_batch(int n, Fn &&fn) {
+    int q0 = 0;
+    while (q0 < n) {
+      const int left = n - q0;
+      if (left >= 8) { fn(std::integral_constant<int, 8>{}, q0); q0 += 8; }
+      else if (left >= 4) { fn(std::integral_constant<int, 4>{}, q0); q0 += 4; }
+      else if (left >= 2) { fn(std::integral_constant<int, 2>{}, q0); q0 += 2; }
+      else { fn(std::integral_constant<int, 1>{}, q0); q0 += 1; }
+    }
+  }
+
   void op(int l, int shifted, const void *x, const void *f, void *y, cudaStream_t s) {
     const Level &Lv = lev[l];
     halo(l, x, l == 0 ? 1 : Lv.r, s);
@@ -677,16 +708,22 @@ template <typename T> struct Solver : SolverBase {
       return;
     }
     const C *cf = Lv.coef.template as<C>();
-    tag(f ? "stored_residual" : "stored_apply", l,
-        kcount(opt.dim, Lv.r) * sizeof(C) * nn + (f ? 3 : 2) * sz * nn);
-    if (opt.dim == 2) {
-      if (Lv.r == 1) launch(k_stored_op<double, T, 2, 1>, nl.grid, nl.block, 0, s, Lv.geo, cf, xx, ff, yy);
-      else if (Lv.r == 2) launch(k_stored_op<double, T, 2, 2>, nl.grid, nl.block, 0, s, Lv.geo, cf, xx, ff, yy);
-      else launch(k_stored_op<double, T, 2, 3>, nl.grid, nl.block, 0, s, Lv.geo, cf, xx, ff, yy);
-    } else {
-      if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1>, nl.grid, nl.block, 0, s, Lv.geo, cf, xx, ff, yy);
-      else launch(k_stored_op<double, T, 3, 2>, nl.grid, nl.block, 0, s, Lv.geo, cf, xx, ff, yy);
-    }
+    const int64_t bs = Lv.geo.total;
+    over_batch(nbat(l), [&](auto NRc, int q0) {
+      constexpr int NR = decltype(NRc)::value;
+      const D *xq = xx + q0 * bs, *fq = ff ? ff + q0 * bs : nullptr;
+      D *yq = yy + q0 * bs;
+      tag(f ? "stored_residual" : "stored_apply", l,
+          kcount(opt.dim, Lv.r) * sizeof(C) * nn + (f ? 3 : 2) * sz * nn * NR);
+      if (opt.dim == 2) {
+        if (Lv.r == 1) launch(k_stored_op<double, T, 2, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
+        else if (Lv.r == 2) launch(k_stored_op<double, T, 2, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
+        else launch(k_stored_op<double, T, 2, 3, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
+      } else {
+        if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
+        else launch(k_stored_op<double, T, 3, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
+      }
+    });
   }
 
   template <typename TI> void restrict_t(int l, const TI *r, D *fc, cudaStream_t s) {
@@ -712,8 +749,12 @@ template <typename T> struct Solver : SolverBase {
     }
   }
   void restrict_(int l, const void *r, void *fc, cudaStream_t s) {
-    if (l == 0) restrict_t<C>(l, (const C *)r, (D *)fc, s);
-    else restrict_t<D>(l, (const D *)r, (D *)fc, s);
+    if (l == 0) {
+      restrict_t<C>(l, (const C *)r, (D *)fc, s);
+      return;
+    }
+    for (int q = 0; q < nrb; ++q)
+      restrict_t<D>(l, (const D *)r + q * lev[l].geo.total, (D *)fc + q * lev[l + 1].geo.total, s);
   }
 
   template <typename TU> void prolong_t(int l, const D *e, const TU *u, TU *uo, cudaStream_t s) {
@@ -739,8 +780,13 @@ template <typename T> struct Solver : SolverBase {
   }
   // u_out = u + P_l e  (u_out may be u)
   void prolong_(int l, const void *e, const void *u, void *u_out, cudaStream_t s) {
-    if (l == 0) prolong_t<C>(l, (const D *)e, (const C *)u, (C *)u_out, s);
-    else prolong_t<D>(l, (const D *)e, (const D *)u, (D *)u_out, s);
+    if (l == 0) {
+      prolong_t<C>(l, (const D *)e, (const C *)u, (C *)u_out, s);
+      return;
+    }
+    const int64_t fs = lev[l].geo.total, cs = lev[l + 1].geo.total;
+    for (int q = 0; q < nrb; ++q)
+      prolong_t<D>(l, (const D *)e + q * cs, (const D *)u + q * fs, (D *)u_out + q * fs, s);
   }
 
   // generic Vanka sweep: the assembled operator B applied as a stencil; TV = level vector type
@@ -751,9 +797,13 @@ template <typename T> struct Solver : SolverBase {
     constexpr int NB = BStencil<DIM, KIND>::NB;
     const double nn = (double)Lv.geo.nodes();
     halo(l, r, 2, s);   // B reaches offsets up to +-2 (RB / Plus)
-    tag(zero ? "vanka_zero" : "vanka", l, ((double)NB * sizeof(C) + (zero ? 2 : 3) * sizeof(TV)) * nn);
-    launch(k_vanka_stencil<BV, T, DIM, KIND>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)Lv.bop.template as<C>(),
-           (const TV *)r, (const TV *)u, (TV *)u, (BV)damp(l), zero);
+    const int64_t bs = Lv.geo.total;
+    over_batch(nbat(l), [&](auto NRc, int q0) {
+      constexpr int NR = decltype(NRc)::value;
+      tag(zero ? "vanka_zero" : "vanka", l, ((double)NB * sizeof(C) + (zero ? 2 : 3) * sizeof(TV) * NR) * nn);
+      launch(k_vanka_stencil<BV, T, DIM, KIND, NR>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)Lv.bop.template as<C>(),
+             (const TV *)r + q0 * bs, (const TV *)u + q0 * bs, (TV *)u + q0 * bs, (BV)damp(l), zero, bs);
+    });
   }
   template <typename TV> void vanka_kind(int l, const void *r, void *u, int zero, cudaStream_t s) {
     const int dim = opt.dim;
@@ -812,7 +862,7 @@ template <typename T> struct Solver : SolverBase {
       }
       return;
     }
-    if (u_out != u && !zero) CK(cudaMemcpyAsync(u_out, u, Lv.geo.total * vsize(l), cudaMemcpyDeviceToDevice, s));
+    if (u_out != u && !zero) CK(cudaMemcpyAsync(u_out, u, Lv.geo.total * vsize(l) * nbat(l), cudaMemcpyDeviceToDevice, s));
     const void *r = f;
     if (!zero) {
       op(l, 1, u_out, f, Lv.r_.p, s);
@@ -835,9 +885,13 @@ template <typename T> struct Solver : SolverBase {
   void coarse_(const void *r, void *e, cudaStream_t s) {
     const Level &Lc = lev[L - 1];
     const int N = (int)Lc.geo.nodes();
-    tag("coarse_gemv", L - 1, (double)N * N * 16 + 2.0 * N * sizeof(D));
-    launch(k_coarse_gemv<double>, dim3((N + 7) / 8), dim3(256), 0, s, Lc.geo, (const D *)ainv.template as<D>(),
-           (const D *)r, (D *)e);
+    const int64_t bs = Lc.geo.total;
+    over_batch(nrb, [&](auto NRc, int q0) {
+      constexpr int NR = decltype(NRc)::value;
+      tag("coarse_gemv", L - 1, (double)N * N * 16 + 2.0 * N * sizeof(D) * NR);
+      launch(k_coarse_gemv<double, NR>, dim3((N + 7) / 8), dim3(256), 0, s, Lc.geo, (const D *)ainv.template as<D>(),
+             (const D *)r + q0 * bs, (D *)e + q0 * bs, bs);
+    });
   }
 
   bool graphs_ok() const { return (!comm || comm->size == 1) && !prof_active() && std::getenv("HMG_NO_GRAPHS") == nullptr; }
@@ -853,19 +907,22 @@ template <typename T> struct Solver : SolverBase {
     }
     CK(cudaEventRecord(gev_in, s));
     CK(cudaStreamWaitEvent(gstream, gev_in, 0));
-    if (!cgraph) {
+    auto it = cgraphs.find(nrb);
+    if (it == cgraphs.end()) {
       const long long k0 = launch_count_now();
       cudaGraph_t gr;
       CK(cudaStreamBeginCapture(gstream, cudaStreamCaptureModeThreadLocal));
       cycle(1, lev[1].f.p, lev[1].u.p, 1, gstream, true);
       CK(cudaStreamEndCapture(gstream, &gr));
-      CK(cudaGraphInstantiate(&cgraph, gr, 0));
+      cudaGraphExec_t ex;
+      CK(cudaGraphInstantiate(&ex, gr, 0));
       CK(cudaGraphDestroy(gr));
-      cgraph_kernels = launch_count_now() - k0;
-      add_launches(-cgraph_kernels);          // captured, not launched
+      cgraph_kernels_nr[nrb] = launch_count_now() - k0;
+      add_launches(-cgraph_kernels_nr[nrb]);          // captured, not launched
+      it = cgraphs.emplace(nrb, ex).first;
     }
-    CK(cudaGraphLaunch(cgraph, gstream));
-    add_launches(cgraph_kernels);
+    CK(cudaGraphLaunch(it->second, gstream));
+    add_launches(cgraph_kernels_nr[nrb]);
     CK(cudaEventRecord(gev_out, gstream));
     CK(cudaStreamWaitEvent(s, gev_out, 0));
   }
@@ -885,7 +942,7 @@ template <typename T> struct Solver : SolverBase {
       if (k == 0 && zero) smooth(l, f, nullptr, u, 1, s);      //   zero guess: r = f, u written only
       else smooth_inplace(l, f, u, s);
     }
-    if (opt.nu1 == 0 && zero) CK(cudaMemsetAsync(u, 0, Lv.geo.total * vsize(l), s));
+    if (opt.nu1 == 0 && zero) CK(cudaMemsetAsync(u, 0, Lv.geo.total * vsize(l) * nbat(l), s));
     op(l, 1, u, f, Lv.r_.p, s);                                // step 2: r = f - A u
     Level &Cc = lev[l + 1];
     restrict_(l, Lv.r_.p, Cc.f.p, s);                          //         f_c = R r
@@ -1086,178 +1143,323 @@ template <typename T> struct Solver : SolverBase {
     }
   }
 
+  // ---------------------------------------------------------------- FGMRES
+  // One right-hand side's Krylov state.  Its device buffers are swapped into the
+  // solver's working members (V, Z, qd, xd, rd) while it is advanced (bind).
+  typedef std::complex<double> cd;
+  struct RhsState {
+    DBuf V, Z, qd, xd, rd;
+    std::vector<cd> H, cs, sn, gv, y;
+    std::vector<double> nbeta, hist;
+    int m = 0, j = 0, its = 0, restarts = 0;
+    bool active = true, converged = false, start = true, have_res = false, failed = false;
+    double qn = 0, true_rel = 1, est = 1;
+    cd &Hs(int i, int k) { return H[(size_t)i * m + k]; }
+  };
+  void bind(RhsState &r) {
+    std::swap(V, r.V);
+    std::swap(Z, r.Z);
+    std::swap(qd, r.qd);
+    std::swap(xd, r.xd);
+    std::swap(rd, r.rd);
+  }
+  // the state's own buffers (the first state of a solve borrows the solver's)
+  void alloc_state(RhsState &r, int m, cudaStream_t s) {
+    const Geo &g = g0();
+    r.V.alloc((size_t)(m + 1) * g.total * sizeof(C), s);
+    r.Z.alloc((size_t)m * g.total * sizeof(C), s);
+    r.qd.alloc(g.total * sizeof(double2), s);
+    r.xd.alloc(g.total * sizeof(double2), s);
+    r.rd.alloc(g.total * sizeof(double2), s);
+  }
+
+  // level 0 of one V-cycle for each of na right-hand sides, levels >= 1 as one
+  // batched pass (coefficients read once for all of them); per right-hand side
+  // the same kernels and arithmetic as cycle(0, ...)
+  void cycle_batch(const std::vector<const C *> &f, const std::vector<C *> &u, cudaStream_t s) {
+    const int na = (int)f.size();
+    if (na == 1 || L < 2) {
+      for (int k = 0; k < na; ++k) cycle(0, f[k], u[k], 1, s);
+      return;
+    }
+    ensure_batch(na, s);
+    Level &F = lev[0], &C1 = lev[1];
+    const int64_t b1 = C1.geo.total;
+    for (int k = 0; k < na; ++k) {
+      for (int i = 0; i < opt.nu1; ++i) {
+        if (i == 0) smooth(0, f[k], nullptr, u[k], 1, s);
+        else smooth_inplace(0, f[k], u[k], s);
+      }
+      if (opt.nu1 == 0) CK(cudaMemsetAsync(u[k], 0, F.geo.total * sizeof(C), s));
+      op(0, 1, u[k], f[k], F.r_.p, s);
+      restrict_(0, F.r_.p, C1.f.template as<D>() + k * b1, s);
+    }
+    nrb = na;
+    const int rec = opt.cycle == 1 ? 2 : 1;
+    for (int c = 0; c < rec; ++c) cycle(1, C1.f.p, C1.u.p, c == 0, s);
+    nrb = 1;
+    for (int k = 0; k < na; ++k) {
+      const D *e = C1.u.template as<D>() + k * b1;
+      if (opt.nu2 > 0 && fused_sweep(0)) {
+        prolong_(0, e, u[k], F.r_.p, s);
+        smooth(0, f[k], F.r_.p, u[k], 0, s);
+        for (int i = 1; i < opt.nu2; ++i) smooth_inplace(0, f[k], u[k], s);
+      } else {
+        prolong_(0, e, u[k], u[k], s);
+        for (int i = 0; i < opt.nu2; ++i) smooth_inplace(0, f[k], u[k], s);
+      }
+    }
+  }
+  // level >= 1 buffers for nr right-hand sides (captured graphs hold the old ones)
+  void ensure_batch(int nr, cudaStream_t s) {
+    if (nr <= nrb_cap) return;
+    for (int l = 1; l < L; ++l) {
+      Level &Lv = lev[l];
+      Lv.u.alloc((size_t)nr * Lv.geo.total * vsize(l), s);
+      Lv.f.alloc((size_t)nr * Lv.geo.total * vsize(l), s);
+      Lv.r_.alloc((size_t)nr * Lv.geo.total * vsize(l), s);
+    }
+    for (auto &kv : cgraphs) cudaGraphExecDestroy(kv.second);
+    cgraphs.clear();
+    nrb_cap = nr;
+  }
+
+  // Start (or restart) the Arnoldi process of a bound state: r = q - H x in fp64,
+  // stop if the true residual already meets tol, else W_0 = r / beta.
+  void fgmres_start(RhsState &r, double tol, cudaStream_t s) {
+    if (!r.have_res) residual_d(s);                   // r = q - H x (fp64)
+    r.have_res = false;
+    const double beta = norm<double>(rd.template as<double2>(), s);
+    r.true_rel = beta / r.qn;
+    if (!std::isfinite(beta)) throw HmgError(HMG_EBREAKDOWN, "non-finite residual norm");
+    if (r.true_rel < tol) {
+      r.converged = true;
+      r.active = false;
+      return;
+    }
+    scale<double, T>(rd.template as<double2>(), Vp(0), 1.0 / beta, s);
+    std::fill(r.H.begin(), r.H.end(), cd(0, 0));
+    std::fill(r.gv.begin(), r.gv.end(), cd(0, 0));
+    r.gv[0] = beta;
+    r.nbeta[0] = 1.0;
+    r.j = 0;
+    r.start = false;
+  }
+
+  // One Arnoldi step j of a bound state after its preconditioner application
+  // z'_j = M(W_j) (already in Z[j]).  Lazily normalised basis: V[j] holds
+  // W_j = nb[j] v_j with nb[j] = ||W_j|| (nb[0] = 1); the cycle and the matvec
+  // run on W_j, so d_i = W_i^H (H M W_j) = nb[i] nb[j] h_ij, the AXPY removes
+  // (d_i / nb[i]^2) W_i, and W_{j+1} = nb[j] w_perp needs no scaling pass.
+  void fgmres_step(RhsState &r, double tol, int maxiter, cudaStream_t s) {
+    const int j = r.j, m = r.m;
+    double2 *dr = dres.template as<double2>();
+    double *ib2h = hpin + 512, *ib2d = reinterpret_cast<double *>(dr + 160);
+    C *w = Vp(j + 1);
+    matvec(Zp(j), w, s);                              // w' = H z'_j (fp64 arithmetic)
+    const int nv = j + 1;
+    for (int i = 0; i <= j; ++i) ib2h[i] = 1.0 / (r.nbeta[i] * r.nbeta[i]);
+    CK(cudaMemcpyAsync(ib2d, ib2h, nv * sizeof(double), cudaMemcpyHostToDevice, s));
+    // classical Gram-Schmidt with selective reorthogonalisation: a second
+    // pass only under strong cancellation, ||w''|| < 0.1 ||w'|| (DESIGN.md
+    // §6: DGKS's 1/sqrt 2 reorthogonalised 59% of the steps at N=4096 and
+    // never changed an iteration count)
+    mdot<T, T>(V.template as<C>(), nv, w, dr, s, true);            // d = W^H w', ||w'||^2
+    maxpy<T, T>(V.template as<C>(), nv, dr, -1.0, w, dr + 64, s, ib2d);   // w'' = w' - W diag(1/nb^2) d
+    CK(cudaMemcpyAsync(hpin, dr, 65 * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double2 *hh = reinterpret_cast<const double2 *>(hpin);
+    for (int i = 0; i <= j; ++i) r.Hs(i, j) = cd(hh[i].x, hh[i].y) / (r.nbeta[i] * r.nbeta[j]);
+    double hn2 = hh[64].x;
+    if (!(hn2 >= kReorthEta2 * hh[nv].x)) {
+      ++reorth;
+      mdot<T, T>(V.template as<C>(), nv, w, dr + 32, s);
+      maxpy<T, T>(V.template as<C>(), nv, dr + 32, -1.0, w, dr + 64, s, ib2d);
+      CK(cudaMemcpyAsync(hpin + 64, dr + 32, 33 * sizeof(double2), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int i = 0; i <= j; ++i) r.Hs(i, j) += cd(hh[32 + i].x, hh[32 + i].y) / (r.nbeta[i] * r.nbeta[j]);
+      hn2 = hh[64].x;
+    }
+    const double wn = std::sqrt(std::max(hn2, 0.0));          // ||W_{j+1}||
+    for (int i = 0; i <= j; ++i)
+      if (!std::isfinite(r.Hs(i, j).real()) || !std::isfinite(r.Hs(i, j).imag()))
+        throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi coefficient");
+    if (!std::isfinite(wn)) throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi norm");
+    const double hn = wn / r.nbeta[j];
+    r.Hs(j + 1, j) = hn;
+    const bool breakdown = hn == 0.0;
+    r.nbeta[j + 1] = wn;
+    if (!breakdown && (wn < 1e-25 || wn > 1e25)) {   // keep the stored basis in range (rare)
+      scale<T, T>(w, w, 1.0 / wn, s);
+      r.nbeta[j + 1] = 1.0;
+    }
+    for (int i = 0; i < j; ++i) {                    // previous Givens rotations
+      const cd t = r.cs[i] * r.Hs(i, j) + r.sn[i] * r.Hs(i + 1, j);
+      r.Hs(i + 1, j) = -std::conj(r.sn[i]) * r.Hs(i, j) + std::conj(r.cs[i]) * r.Hs(i + 1, j);
+      r.Hs(i, j) = t;
+    }
+    const cd a = r.Hs(j, j), b = r.Hs(j + 1, j);
+    const double den = std::sqrt(std::norm(a) + std::norm(b));
+    if (den == 0.0) { r.cs[j] = 1.0; r.sn[j] = 0.0; }
+    else if (std::abs(a) == 0.0) { r.cs[j] = 0.0; r.sn[j] = 1.0; }
+    else { r.cs[j] = std::abs(a) / den; r.sn[j] = (a / std::abs(a)) * std::conj(b) / den; }
+    r.Hs(j, j) = r.cs[j] * a + r.sn[j] * b;
+    r.Hs(j + 1, j) = 0.0;
+    r.gv[j + 1] = -std::conj(r.sn[j]) * r.gv[j];
+    r.gv[j] = r.cs[j] * r.gv[j];
+    ++r.its;
+    r.est = std::abs(r.gv[j + 1]) / r.qn;
+    r.hist.push_back(r.est);
+    const bool stop = r.est < tol || breakdown || r.its >= maxiter;
+    if (!stop && j + 1 < m) {
+      r.j = j + 1;
+      return;
+    }
+    // end of a restart cycle: x += Z y (fp64), then the fp64 true residual
+    const int jend = j + 1;
+    for (int i = jend - 1; i >= 0; --i) {           // back substitution
+      cd acc = r.gv[i];
+      for (int k = i + 1; k < jend; ++k) acc -= r.Hs(i, k) * r.y[k];
+      r.y[i] = acc / r.Hs(i, i);
+    }
+    double2 *yp = reinterpret_cast<double2 *>(hpin) + 128;
+    for (int i = 0; i < jend; ++i) yp[i] = make_double2(r.y[i].real() / r.nbeta[i], r.y[i].imag() / r.nbeta[i]);
+    CK(cudaMemcpyAsync(dr + 96, yp, jend * sizeof(double2), cudaMemcpyHostToDevice, s));
+    maxpy<T, double>(Z.template as<C>(), jend, dr + 96, 1.0, xd.template as<double2>(), nullptr, s);
+    ++r.restarts;
+    residual_d(s);
+    r.have_res = true;
+    r.start = true;
+    if (stop) {
+      r.true_rel = norm<double>(rd.template as<double2>(), s) / r.qn;
+      if (r.true_rel < tol) { r.converged = true; r.active = false; return; }
+    }
+    if (r.its >= maxiter) r.active = false;
+  }
+
   // Saad's FGMRES(m) with CGS2 Arnoldi and complex Givens rotations; x0 = 0;
   // stop when |g_{j+1}|/||q|| < tol and the fp64 true residual confirms it
-  // (reading A17), else restart.  Solves qd -> xd.
-  hmg_status fgmres(int m, double tol, int maxiter, cudaStream_t s, std::vector<double> &hist, int &its_out,
-                    int &restarts_out, double &true_rel_out, double &est_out) {
-    typedef std::complex<double> cd;
+  // (reading A17), else restart.  Every state solves its qd -> xd; the states
+  // advance in lockstep, one batched preconditioner application per step.
+  void fgmres(std::vector<RhsState> &st, int m, double tol, int maxiter, cudaStream_t s) {
     ensure_ws(m, s);
-    const Geo &g = g0();
-    double2 *x = xd.template as<double2>();
-    CK(cudaMemsetAsync(x, 0, g.total * sizeof(double2), s));
-    const double qn = norm<double>(qd.template as<double2>(), s);
-    hist.assign(1, 1.0);
-    int its = 0, restarts = 0;
-    bool converged = false;
-    double true_rel = 1.0, est = 1.0;
-    if (qn == 0.0) {
-      its_out = 0; restarts_out = 0; true_rel_out = 0.0; est_out = 0.0;
-      return HMG_OK;
-    }
-    std::vector<cd> H((m + 1) * m), cs(m), sn(m), gv(m + 1), y(m);
-    std::vector<double> nbeta(m + 1, 1.0);
-    auto Hs = [&](int i, int j) -> cd & { return H[(size_t)i * m + j]; };
-    double2 *dr = dres.template as<double2>();
-    bool have_res = false;
     reorth = 0;
-    while (its < maxiter) {
-      if (!have_res) residual_d(s);                   // r = q - H x (fp64)
-      have_res = false;
-      const double beta = norm<double>(rd.template as<double2>(), s);
-      true_rel = beta / qn;
-      if (!std::isfinite(beta)) throw HmgError(HMG_EBREAKDOWN, "non-finite residual norm");
-      if (true_rel < tol) { converged = true; break; }
-      scale<double, T>(rd.template as<double2>(), Vp(0), 1.0 / beta, s);
-      std::fill(H.begin(), H.end(), cd(0, 0));
-      std::fill(gv.begin(), gv.end(), cd(0, 0));
-      gv[0] = beta;
-      // Lazily normalised Arnoldi basis: V[j] holds W_j = nb[j] v_j with
-      // nb[j] = ||W_j|| (nb[0] = 1); the cycle and the matvec run on W_j, so
-      // d_i = W_i^H (H M W_j) = nb[i] nb[j] h_ij, the AXPY removes
-      // (d_i / nb[i]^2) W_i, and W_{j+1} = nb[j] w_perp needs no scaling pass.
-      nbeta[0] = 1.0;
-      int jend = 0;
-      bool stop = false;
-      double *ib2h = hpin + 512, *ib2d = reinterpret_cast<double *>(dr + 160);
-      for (int j = 0; j < m; ++j) {
-        cycle(0, Vp(j), Zp(j), 1, s);                // z'_j = M(W_j)
-        C *w = Vp(j + 1);
-        matvec(Zp(j), w, s);                         // w' = H z'_j (fp64 arithmetic)
-        const int nv = j + 1;
-        for (int i = 0; i <= j; ++i) ib2h[i] = 1.0 / (nbeta[i] * nbeta[i]);
-        CK(cudaMemcpyAsync(ib2d, ib2h, nv * sizeof(double), cudaMemcpyHostToDevice, s));
-        // classical Gram-Schmidt with selective reorthogonalisation: a second
-        // pass only under strong cancellation, ||w''|| < 0.1 ||w'|| (DESIGN.md
-        // §6: DGKS's 1/sqrt 2 reorthogonalised 59% of the steps at N=4096 and
-        // never changed an iteration count)
-        mdot<T, T>(V.template as<C>(), nv, w, dr, s, true);            // d = W^H w', ||w'||^2
-        maxpy<T, T>(V.template as<C>(), nv, dr, -1.0, w, dr + 64, s, ib2d);   // w'' = w' - W diag(1/nb^2) d
-        CK(cudaMemcpyAsync(hpin, dr, 65 * sizeof(double2), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        const double2 *hh = reinterpret_cast<const double2 *>(hpin);
-        for (int i = 0; i <= j; ++i) Hs(i, j) = cd(hh[i].x, hh[i].y) / (nbeta[i] * nbeta[j]);
-        double hn2 = hh[64].x;
-        if (!(hn2 >= kReorthEta2 * hh[nv].x)) {
-          ++reorth;
-          mdot<T, T>(V.template as<C>(), nv, w, dr + 32, s);
-          maxpy<T, T>(V.template as<C>(), nv, dr + 32, -1.0, w, dr + 64, s, ib2d);
-          CK(cudaMemcpyAsync(hpin + 64, dr + 32, 33 * sizeof(double2), cudaMemcpyDeviceToHost, s));
-          CK(cudaStreamSynchronize(s));
-          for (int i = 0; i <= j; ++i) Hs(i, j) += cd(hh[32 + i].x, hh[32 + i].y) / (nbeta[i] * nbeta[j]);
-          hn2 = hh[64].x;
+    for (auto &r : st) {
+      r.m = m;
+      r.H.assign((size_t)(m + 1) * m, cd(0, 0));
+      r.cs.assign(m, cd(0, 0));
+      r.sn.assign(m, cd(0, 0));
+      r.gv.assign(m + 1, cd(0, 0));
+      r.y.assign(m, cd(0, 0));
+      r.nbeta.assign(m + 1, 1.0);
+      r.hist.assign(1, 1.0);
+      bind(r);
+      CK(cudaMemsetAsync(xd.p, 0, g0().total * sizeof(double2), s));
+      r.qn = norm<double>(qd.template as<double2>(), s);
+      bind(r);
+      if (r.qn == 0.0) { r.active = false; r.converged = true; r.true_rel = 0.0; r.est = 0.0; }
+      if (maxiter == 0) r.active = false;
+    }
+    std::vector<const C *> fv;
+    std::vector<C *> uv;
+    std::vector<RhsState *> act;
+    for (;;) {
+      act.clear();
+      for (auto &r : st) {
+        if (!r.active) continue;
+        if (r.start) {
+          bind(r);
+          fgmres_start(r, tol, s);
+          bind(r);
         }
-        const double wn = std::sqrt(std::max(hn2, 0.0));          // ||W_{j+1}||
-        for (int i = 0; i <= j; ++i)
-          if (!std::isfinite(Hs(i, j).real()) || !std::isfinite(Hs(i, j).imag()))
-            throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi coefficient");
-        if (!std::isfinite(wn)) throw HmgError(HMG_EBREAKDOWN, "non-finite Arnoldi norm");
-        const double hn = wn / nbeta[j];
-        Hs(j + 1, j) = hn;
-        const bool breakdown = hn == 0.0;
-        nbeta[j + 1] = wn;
-        if (!breakdown && (wn < 1e-25 || wn > 1e25)) {   // keep the stored basis in range (rare)
-          scale<T, T>(w, w, 1.0 / wn, s);
-          nbeta[j + 1] = 1.0;
-        }
-        for (int i = 0; i < j; ++i) {                // previous Givens rotations
-          const cd t = cs[i] * Hs(i, j) + sn[i] * Hs(i + 1, j);
-          Hs(i + 1, j) = -std::conj(sn[i]) * Hs(i, j) + std::conj(cs[i]) * Hs(i + 1, j);
-          Hs(i, j) = t;
-        }
-        const cd a = Hs(j, j), b = Hs(j + 1, j);
-        const double den = std::sqrt(std::norm(a) + std::norm(b));
-        if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; }
-        else if (std::abs(a) == 0.0) { cs[j] = 0.0; sn[j] = 1.0; }
-        else { cs[j] = std::abs(a) / den; sn[j] = (a / std::abs(a)) * std::conj(b) / den; }
-        Hs(j, j) = cs[j] * a + sn[j] * b;
-        Hs(j + 1, j) = 0.0;
-        gv[j + 1] = -std::conj(sn[j]) * gv[j];
-        gv[j] = cs[j] * gv[j];
-        ++its;
-        est = std::abs(gv[j + 1]) / qn;
-        hist.push_back(est);
-        jend = j + 1;
-        if (est < tol || breakdown || its >= maxiter) { stop = true; break; }
+        if (r.active) act.push_back(&r);
       }
-      for (int i = jend - 1; i >= 0; --i) {           // back substitution
-        cd acc = gv[i];
-        for (int k = i + 1; k < jend; ++k) acc -= Hs(i, k) * y[k];
-        y[i] = acc / Hs(i, i);
+      if (act.empty()) break;
+      fv.clear();
+      uv.clear();
+      for (RhsState *r : act) {                       // z'_j = M(W_j) for every active state
+        fv.push_back(r->V.template as<C>() + (size_t)r->j * g0().total);
+        uv.push_back(r->Z.template as<C>() + (size_t)r->j * g0().total);
       }
-      double2 *yp = reinterpret_cast<double2 *>(hpin) + 128;
-      for (int i = 0; i < jend; ++i) yp[i] = make_double2(y[i].real() / nbeta[i], y[i].imag() / nbeta[i]);  // z_i = z'_i / nb[i]
-      CK(cudaMemcpyAsync(dr + 96, yp, jend * sizeof(double2), cudaMemcpyHostToDevice, s));
-      maxpy<T, double>(Z.template as<C>(), jend, dr + 96, 1.0, x, nullptr, s);   // x += Z y (fp64)
-      ++restarts;
-      residual_d(s);
-      have_res = true;
-      if (stop) {
-        true_rel = norm<double>(rd.template as<double2>(), s) / qn;
-        if (true_rel < tol) { converged = true; break; }
+      cycle_batch(fv, uv, s);
+      for (RhsState *r : act) {
+        bind(*r);
+        fgmres_step(*r, tol, maxiter, s);
+        bind(*r);
       }
     }
-    its_out = its;
-    restarts_out = restarts;
-    true_rel_out = true_rel;
-    est_out = est;
-    return converged ? HMG_OK : HMG_ENOTCONVERGED;
+  }
+
+  void fill_report(const RhsState &r, float ms, hmg_report *rep) {
+    rep->iterations = r.its;
+    rep->converged = r.converged;
+    rep->restarts = r.restarts;
+    rep->relres_true = r.true_rel;
+    rep->relres_est = r.est;
+    rep->seconds = ms * 1e-3;
+    const int n = (int)r.hist.size();
+    rep->history_len = rep->history ? std::min(n, rep->history_cap) : 0;
+    for (int i = 0; i < rep->history_len; ++i) rep->history[i] = r.hist[i];
+    // c_f of Eq. 5.1 after a 5-iteration warm-up
+    const int wu = 5;
+    if (n > wu + 1) rep->c_f = std::pow(r.hist[n - 1] / r.hist[wu], 1.0 / (n - 1 - wu));
+    else rep->c_f = std::nan("");
   }
 
   hmg_status api_fgmres(const void *q, void *x, int host, int m, double tol, int maxiter, cudaStream_t s,
                         hmg_report *rep) override {
+    return api_fgmres_batch(1, q, x, host, m, tol, maxiter, s, rep);
+  }
+
+  // nr right-hand sides q[k * N ...], solutions x[k * N ...] (unpadded, contiguous)
+  hmg_status api_fgmres_batch(int nr, const void *q, void *x, int host, int m, double tol, int maxiter,
+                              cudaStream_t s, hmg_report *reps) override {
     if (m < 1 || m >= KRY_MAXV) throw HmgError(HMG_EINVAL, "restart must be in [1, 31]");
     if (!(tol > 0) || maxiter < 0) throw HmgError(HMG_EINVAL, "tol must be > 0 and maxiter >= 0");
+    if (nr < 1) throw HmgError(HMG_EINVAL, "nrhs must be >= 1");
+    if (nr > 1 && comm && comm->size > 1) throw HmgError(HMG_EINVAL, "batched solves run on one rank");
+    if (nr > 1 && host) throw HmgError(HMG_EINVAL, "batched solves take device buffers");
     ensure_ws(m, s);
     const Geo &g = g0();
     const int64_t N = g.nodes();
     auto nl = node_launch(g);
-    const C *qsrc = (const C *)q;
-    if (host) {
-      CK(cudaMemcpyAsync(io.p, q, N * sizeof(C), cudaMemcpyHostToDevice, s));
-      qsrc = io.template as<C>();
+    std::vector<RhsState> st(nr);
+    bind(st[0]);                                      // the first state borrows the solver's buffers
+    for (int k = 1; k < nr; ++k) alloc_state(st[k], m, s);
+    for (int k = 0; k < nr; ++k) {
+      const C *qsrc = (const C *)q + (size_t)k * N;
+      if (host) {
+        CK(cudaMemcpyAsync(io.p, q, N * sizeof(C), cudaMemcpyHostToDevice, s));
+        qsrc = io.template as<C>();
+      }
+      tag("pack", 0, (double)(sizeof(C) + sizeof(double2)) * N);
+      launch(k_pack_cvt<T, double>, nl.grid, nl.block, 0, s, g, qsrc, 0, st[k].qd.template as<double2>(), 1);
     }
-    tag("pack", 0, (double)(sizeof(C) + sizeof(double2)) * N);
-    launch(k_pack_cvt<T, double>, nl.grid, nl.block, 0, s, g, qsrc, 0, qd.template as<double2>(), 1);
     CK(cudaEventRecord(ev0, s));
-    std::vector<double> hist;
-    int its = 0, restarts = 0;
-    double tr = 0, est = 0;
-    hmg_status st = fgmres(m, tol, maxiter, s, hist, its, restarts, tr, est);
+    hmg_status st_out = HMG_OK;
+    try {
+      fgmres(st, m, tol, maxiter, s);
+    } catch (...) {
+      bind(st[0]);                                    // give the borrowed buffers back
+      throw;
+    }
     CK(cudaEventRecord(ev1, s));
-    C *xdst = host ? io.template as<C>() : (C *)x;
-    tag("unpack", 0, (double)(sizeof(C) + sizeof(double2)) * N);
-    launch(k_pack_cvt<double, T>, nl.grid, nl.block, 0, s, g, (const double2 *)xd.template as<double2>(), 1, xdst, 0);
-    if (host) CK(cudaMemcpyAsync(x, io.p, N * sizeof(C), cudaMemcpyDeviceToHost, s));
+    for (int k = 0; k < nr; ++k) {
+      C *xdst = host ? io.template as<C>() : (C *)x + (size_t)k * N;
+      tag("unpack", 0, (double)(sizeof(C) + sizeof(double2)) * N);
+      launch(k_pack_cvt<double, T>, nl.grid, nl.block, 0, s, g, (const double2 *)st[k].xd.template as<double2>(), 1,
+             xdst, 0);
+      if (host) CK(cudaMemcpyAsync(x, io.p, N * sizeof(C), cudaMemcpyDeviceToHost, s));
+      if (!st[k].converged) st_out = HMG_ENOTCONVERGED;
+    }
     CK(cudaStreamSynchronize(s));
-    if (rep) {
+    bind(st[0]);                                      // give the borrowed buffers back
+    if (reps) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, ev0, ev1));
-      rep->iterations = its;
-      rep->converged = st == HMG_OK;
-      rep->restarts = restarts;
-      rep->relres_true = tr;
-      rep->relres_est = est;
-      rep->seconds = ms * 1e-3;
-      const int n = (int)hist.size();
-      rep->history_len = rep->history ? std::min(n, rep->history_cap) : 0;
-      for (int i = 0; i < rep->history_len; ++i) rep->history[i] = hist[i];
-      // c_f of Eq. 5.1 after a 5-iteration warm-up
-      const int wu = 5;
-      if (n > wu + 1) rep->c_f = std::pow(hist[n - 1] / hist[wu], 1.0 / (n - 1 - wu));
-      else rep->c_f = std::nan("");
+      for (int k = 0; k < nr; ++k) fill_report(st[k], ms, reps + k);
     }
-    return st;
+    return st_out;
   }
 
   // ------------------------------------------------------------ introspection
@@ -1512,6 +1714,16 @@ hmg_status hmg_fgmres_solve_host(const hmg_hierarchy *h, const void *q, void *x,
   if (!h || !q || !x) return fail(HMG_EINVAL, "null pointer");
   hmg_status st = h->impl->api_fgmres(q, x, 1, restart, tol, maxiter, S(stream), rep);
   if (st == HMG_ENOTCONVERGED) t_err = "FGMRES reached maxiter without converging";
+  return st;
+  HMG_API_END
+}
+
+hmg_status hmg_fgmres_solve_batch(const hmg_hierarchy *h, int nrhs, const void *q, void *x, int restart, double tol,
+                                  int maxiter, void *stream, hmg_report *reps) {
+  HMG_API_BEGIN
+  if (!h || !q || !x) return fail(HMG_EINVAL, "null pointer");
+  hmg_status st = h->impl->api_fgmres_batch(nrhs, q, x, 0, restart, tol, maxiter, S(stream), reps);
+  if (st == HMG_ENOTCONVERGED) t_err = "FGMRES reached maxiter without converging for at least one right-hand side";
   return st;
   HMG_API_END
 }

@@ -153,16 +153,20 @@ __global__ void __launch_bounds__(256) k_fine_op2d_pair(Geo g, const cplx<TSG> *
 // Stored stencil of radius R: coef[k][j], k = (ox+R) + (2R+1)((oy+R) + (2R+1)(oz+R)),
 // multiplies x[j + o].  Coefficients towards out-of-domain nodes are zero.
 // TV = vector storage/arithmetic (fp64 on Galerkin levels), TK = coefficient storage.
-template <typename TV, typename TK, int DIM, int R>
+template <typename TV, typename TK, int DIM, int R, int NR = 1>
 __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__restrict__ coef,
                                                    const cplx<TV> *__restrict__ x,
-                                                   const cplx<TV> *__restrict__ f, cplx<TV> *__restrict__ y) {
+                                                   const cplx<TV> *__restrict__ f, cplx<TV> *__restrict__ y,
+                                                   int64_t bs = 0) {
+  // NR right-hand sides at a stride of bs elements: each coefficient is read once
+  // and applied to all of them (multi-RHS batches; same per-RHS arithmetic order)
   using T = TV;
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t i = g.idx(ix, iy, iz);
-  constexpr int W = 2 * R + 1;
   constexpr int ZR = DIM == 3 ? R : 0;
-  cplx<T> acc = mkc<T>(0, 0);
+  cplx<T> acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = mkc<T>(0, 0);
   int k = 0;
 #pragma unroll
   for (int oz = -ZR; oz <= ZR; ++oz)
@@ -171,10 +175,12 @@ __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__rest
 #pragma unroll
       for (int ox = -R; ox <= R; ++ox, ++k) {
         const cplx<T> c = ccast<T, TK>(coef[(int64_t)k * g.total + i]);
-        acc = cfma<T>(acc, c, x[i + g.delta(ox, oy, oz)]);
+        const int64_t j = i + g.delta(ox, oy, oz);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[r] = cfma<T>(acc[r], c, x[r * bs + j]);
       }
-  (void)W;
-  y[i] = f ? csub<T>(f[i], acc) : acc;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) y[r * bs + i] = f ? csub<T>(f[r * bs + i], acc[r]) : acc[r];
 }
 
 }  // namespace hmg

@@ -67,6 +67,9 @@ template <int DIM, int KIND> struct Patch {
   }
 };
 
+__device__ __forceinline__ double __fmul_rn_t(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float __fmul_rn_t(float a, float b) { return __fmul_rn(a, b); }
+
 // 1 / cnt_j for cnt_j = 1..8 (a table instead of a per-node fp64 division)
 __constant__ double kInvCount[9] = {0.0, 1.0, 0.5, 1.0 / 3.0, 0.25, 0.2, 1.0 / 6.0, 1.0 / 7.0, 0.125};
 
@@ -132,21 +135,36 @@ __device__ __forceinline__ void static_for(F &&f) {
 // u_out_j = u_j + w sum_p B[p][j] r[j + d_p]   (u unused when zero; in place is safe:
 // every node reads and writes only its own u).  B vanishes at non-anchor /
 // out-of-domain positions and r is zero (ghosts) or exchanged (halo) there.
-template <typename T, typename TK, int DIM, int KIND>
+template <typename T, typename TK, int DIM, int KIND, int NR = 1>
 __global__ void __launch_bounds__(256) k_vanka_stencil(Geo g, const cplx<TK> *__restrict__ B,
                                                        const cplx<T> *__restrict__ r, const cplx<T> *u,
-                                                       cplx<T> *u_out, T w, int zero) {
+                                                       cplx<T> *u_out, T w, int zero, int64_t bs = 0) {
   HMG_NODE_IDX(g, ix, iy, iz);
   using S = BStencil<DIM, KIND>;
   const int64_t j = g.idx(ix, iy, iz);
-  cplx<T> acc = mkc<T>(0, 0);
+  cplx<T> acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = mkc<T>(0, 0);
   static_for<0, S::NB>([&](auto P) {
     constexpr int p = decltype(P)::value;
     const cplx<T> b = ccast<T, TK>(B[(int64_t)p * g.total + j]);
-    acc = cfma<T>(acc, b, r[j + g.delta(S::template dx<p>, S::template dy<p>, S::template dz<p>)]);
+    const int64_t o = j + g.delta(S::template dx<p>, S::template dy<p>, S::template dz<p>);
+#pragma unroll
+    for (int q = 0; q < NR; ++q) acc[q] = cfma<T>(acc[q], b, r[q * bs + o]);
   });
-  const cplx<T> upd = cscale<T>(acc, w);
-  u_out[j] = zero ? upd : cadd<T>(u[j], upd);
+  // explicit fma / mul: the same rounding in every batch-width instantiation
+  // (left to the compiler, u + w acc is contracted in some and not in others)
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    cplx<T> o;
+    if (zero) {
+      o = mkc<T>(__fmul_rn_t(acc[q].x, w), __fmul_rn_t(acc[q].y, w));
+    } else {
+      const cplx<T> uq = u[q * bs + j];
+      o = mkc<T>(fma(acc[q].x, w, uq.x), fma(acc[q].y, w, uq.y));
+    }
+    u_out[q * bs + j] = o;
+  }
 }
 
 // (1b) fine-level RB smoothing sweep in ONE kernel (2D, matrix-free).

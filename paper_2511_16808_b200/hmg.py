@@ -69,6 +69,7 @@ _sigs = {
     "hmg_vcycle": ([_vp, _vp, _vp, _i, _vp], _i),
     "hmg_fgmres_solve": ([_vp, _vp, _vp, _i, _d, _i, _vp, ctypes.POINTER(_Report)], _i),
     "hmg_fgmres_solve_host": ([_vp, _vp, _vp, _i, _d, _i, _vp, ctypes.POINTER(_Report)], _i),
+    "hmg_fgmres_solve_batch": ([_vp, _i, _vp, _vp, _i, _d, _i, _vp, ctypes.POINTER(_Report)], _i),
     "hmg_num_levels": ([_vp], _i),
     "hmg_level_nodes": ([_vp, _i, ctypes.POINTER(_i64)], _i64),
     "hmg_stencil_radius": ([_vp, _i], _i),
@@ -362,6 +363,30 @@ class Hierarchy:
                 raise ValueError("expected contiguous host tensors of the hierarchy's dtype and size")
         return self._solve(_lib.hmg_fgmres_solve_host, ctypes.c_void_p(q.data_ptr()),
                            ctypes.c_void_p(x.data_ptr()), restart, tol, maxiter, stream, history_cap)
+
+    def fgmres_solve_batch(self, q, x, restart=10, tol=1e-6, maxiter=500, stream=None, history_cap=20000):
+        """nrhs independent solves H x_k = q_k on this hierarchy, advanced in lockstep
+        with one batched preconditioner per step (hmg_fgmres_solve_batch).  q, x: CUDA
+        tensors of shape (nrhs, N) (or nrhs * N contiguous).  Returns a list of Reports."""
+        n = self._n(0)
+        if q.numel() % n or q.numel() != x.numel():
+            raise ValueError("q and x must hold nrhs * N values")
+        nr = q.numel() // n
+        _ptr(q.view(-1), self.dtype, nr * n)   # contiguous CUDA tensors of the hierarchy's dtype
+        _ptr(x.view(-1), self.dtype, nr * n)
+        hists = [(ctypes.c_double * history_cap)() for _ in range(nr)]
+        reps = (_Report * nr)()
+        for k in range(nr):
+            reps[k].history = ctypes.cast(hists[k], ctypes.POINTER(ctypes.c_double))
+            reps[k].history_cap = history_cap
+        st = _lib.hmg_fgmres_solve_batch(self._h, nr, ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(x.data_ptr()),
+                                         int(restart), float(tol), int(maxiter), _stream(stream), reps)
+        if st not in (OK, ENOTCONVERGED):
+            _check(st)
+        return [Report(iterations=r.iterations, converged=bool(r.converged), restarts=r.restarts,
+                       history=list(h[:r.history_len]), relres_true=r.relres_true, relres_est=r.relres_est,
+                       c_f=r.c_f, seconds=r.seconds, status=OK if r.converged else ENOTCONVERGED)
+                for r, h in zip(reps, hists)]
 
     def _solve(self, fn, qp, xp, restart, tol, maxiter, stream, history_cap):
         hist = (ctypes.c_double * history_cap)()
