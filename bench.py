@@ -195,6 +195,11 @@ def run_ours(args):
            "h2d_bytes_per_step": qh.numel() * qh.element_size(),
            "d2h_bytes_per_step": xh.numel() * xh.element_size()}
 
+    # ---------------------------------------------------------------- multi-RHS batch
+    multi = None
+    if ws == 1 and args.nrhs > 1:
+        multi = multi_rhs(gh, p, n, args, cdt, stream, value)
+
     # ---------------------------------------------------------------- live per-kernel roofline (one extra solve)
     hmg.profile_begin()
     gh.fgmres_solve(q, x, restart=RESTART, tol=TOL, maxiter=args.maxiter)
@@ -242,12 +247,46 @@ def run_ours(args):
         "kernel_launches_per_step": int(sum(v["launches"] for v in prof.values())),
         "kernels": table,
     }
+    if multi:
+        out["multi_rhs"] = multi
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.cpu_n, args.cpu_iters)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def multi_rhs(gh, p, n, args, cdt, stream, single_value):
+    """nrhs point sources at seeded positions in the interior (many shots on one
+    medium) solved as ONE batch (hmg_fgmres_solve_batch): one warm-up
+    batch, one timed batch (CUDA events).  Aggregate unknown-updates/s over all
+    right-hand sides, and the ratio to the single-RHS value of the same run."""
+    import numpy as np
+    import torch
+    rng = np.random.default_rng(11)
+    N = p.n
+    Q = np.zeros((args.nrhs, N), np.complex128)
+    Q[0] = p.q.ravel()
+    nodes = n + 1
+    for k in range(1, args.nrhs):
+        ix, iy = rng.integers(32, nodes - 32, size=2)
+        Q[k, iy * nodes + ix] = p.q.ravel().max()
+    q = torch.from_numpy(Q).to(cdt).cuda()
+    x = torch.zeros_like(q)
+    gh.fgmres_solve_batch(q, x, restart=RESTART, tol=TOL, maxiter=args.maxiter)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    reps = gh.fgmres_solve_batch(q, x, restart=RESTART, tol=TOL, maxiter=args.maxiter)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    its = [r.iterations for r in reps]
+    v = N * sum(its) / (ms * 1e-3)
+    return {"nrhs": args.nrhs, "value": v, "unit": UNIT, "batch_time_s": ms * 1e-3, "iterations": its,
+            "converged": all(r.converged for r in reps), "vs_single_rhs": round(v / single_value, 3),
+            "sources": "config-1 centre source + seeded interior point sources (numpy default_rng(11))"}
 
 
 _ORACLE = {}
@@ -320,6 +359,7 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=512)
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nrhs", type=int, default=4, help="batch size of the multi-RHS line (<= 1: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
