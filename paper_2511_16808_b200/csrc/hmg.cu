@@ -853,6 +853,22 @@ template <typename T> struct Solver : SolverBase {
       };
       // c64 non-zero: 3 blocks/SM (80 registers) measured 16 % faster than 2 (91 registers)
       constexpr int MB = sizeof(T) == 4 ? 3 : 2;
+      static const bool two = std::getenv("HMG_MARCH1") == nullptr;
+      if (std::is_same<T, float>::value && pair_ok() && c4 && two) {   // two columns per lane
+        const int ns2 = (Lv.geo.n[0] + RB2_STRIP - 1) / RB2_STRIP;
+        const int64_t w2 = (int64_t)ns2 * nsegs;
+        const dim3 grid2((unsigned)((w2 + 3) / 4)), block2(128);
+        auto go2 = [&](auto kern, int na) {
+          const int smem = 4 * (PD + 2) * na * 32 * 16;
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          launch(kern, grid2, block2, (size_t)smem, s, Lv.geo, (const float2 *)sg, (const float2 *)ia,
+                 (const float2 *)id, alpha, ih2, (const float2 *)ff, (const float2 *)ui, (float2 *)uo, w);
+        };
+        // blocks/SM: zero sweep 4 (126 registers), non-zero 3 (152; 4 spills, measured 2.9x slower)
+        if (zero) go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD>, 3);
+        else go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD>, 5);
+        return;
+      }
       if (zero) {
         if (c4) go(k_rb2d_march<T, ST_COMPACT4, true, SEG, double, double, 1, 2, PD>, 3);
         else go(k_rb2d_march<T, ST_FD2, true, SEG, double, double, 1, 2, PD>, 3);

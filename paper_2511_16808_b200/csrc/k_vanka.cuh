@@ -390,4 +390,182 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
   }
 }
 
+// (1b'') the same sweep with TWO columns per lane (c64): a warp owns a strip of 64
+// columns (56 outputs, 4 halo columns per side, x0 even so pairs load as 16 bytes).
+// Per node the arithmetic is exactly that of k_rb2d_march; the per-lane work that
+// does not depend on the node count (shuffles of a row, addresses, ring traffic,
+// loop and predicate logic) is shared by the two nodes.
+constexpr int RB2_STRIP = 56;
+
+template <int KIND, bool ZERO, int SEG, typename TR, int MINB, int PD>
+__global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *__restrict__ sig,
+                                                           const float2 *__restrict__ ia_,
+                                                           const float2 *__restrict__ id_, double alpha_d,
+                                                           double ih2_d, const float2 *__restrict__ f,
+                                                           const float2 *__restrict__ u, float2 *__restrict__ u_out,
+                                                           double w_d) {
+  using W = FineW<2, KIND>;
+  using D = double;
+  using CD = double2;
+  using CS = float2;
+  const D ih2 = ih2_d, w = w_d;
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nstrips = (g.n[0] + RB2_STRIP - 1) / RB2_STRIP;
+  const int strip = wid % nstrips, seg = wid / nstrips;
+  const int y0 = seg * SEG;
+  if (y0 >= g.n[1]) return;
+  const int y1 = min(g.n[1], y0 + SEG);
+  const int x0 = strip * RB2_STRIP - 4 + 2 * lane;   // this lane's columns x0 (node 0) and x0 + 1 (node 1)
+  const bool out_lane = lane >= 2 && lane < 30;
+  bool outn[2], xin[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    outn[q] = out_lane && x0 + q < g.n[0];
+    xin[q] = x0 + q + g.o[0] >= 0 && x0 + q + g.o[0] < g.N[0];
+  }
+  const D e = W::Le * ih2;
+  const CD z = mkc<D>(0, 0);
+  const CS zs = mkc<float>(0, 0);
+  const int ylo = -g.o[1], yhi = g.N[1] - g.o[1];
+  auto yok = [&](int y) { return y >= ylo && y < yhi; };
+  CS um1[2] = {zs, zs}, u0[2] = {zs, zs}, up1[2] = {zs, zs}, ub1[2] = {zs, zs};
+  CD r2[2] = {z, z}, r1[2] = {z, z}, r0[2] = {z, z};
+  CD h2[2] = {z, z}, h1[2] = {z, z}, h0[2] = {z, z};
+  CS a2[2] = {zs, zs}, a1[2] = {zs, zs}, a0[2] = {zs, zs};
+  CD c2[2] = {z, z}, c1[2] = {z, z};
+  CD g3[2] = {z, z}, g2[2] = {z, z}, g1[2] = {z, z};
+  const int64_t px = g.px;
+  int64_t ob = g.base + x0 + (int64_t)(y0 - 2) * px;
+  // valid bytes of this lane's pair in row y (the left domain edge is at an even x)
+  auto nbytes = [&](int y) { return yok(y) ? (xin[1] ? 16 : (xin[0] ? 8 : 0)) : 0; };
+  auto ld2 = [&](const CS *a, int y, int64_t o, CS &v0, CS &v1) {
+    const int nb = nbytes(y);
+    v0 = nb >= 8 ? a[o] : zs;
+    v1 = nb >= 16 ? a[o + 1] : zs;
+  };
+  if (!ZERO) {
+    ld2(u, y0 - 3, ob - px, u0[0], u0[1]);
+    ld2(u, y0 - 2, ob, up1[0], up1[1]);
+  }
+  constexpr int NA = ZERO ? 3 : 5;   // f, ia, id (+ u, sigma)
+  constexpr int NST = PD + 2;
+  extern __shared__ __align__(16) unsigned char rb_smem[];
+  float4 *ring = reinterpret_cast<float4 *>(rb_smem) + (size_t)(threadIdx.x >> 5) * (NST * NA * 32);
+  const int64_t ob0 = ob;
+  auto cp = [&](const CS *a, int y, int64_t o, int slot, int k) {
+    const int nb = nbytes(y);
+    const CS *gp = nb ? a + o : a;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(ring + (slot * NA + k) * 32 + lane);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gp), "r"(nb) : "memory");
+  };
+  auto issue = [&](int it_) {
+    const int b_ = y0 - 2 + it_, slot = it_ % NST;
+    const int64_t o = ob0 + (int64_t)it_ * px;
+    cp(f, b_, o, slot, 0);
+    cp(ia_, b_, o, slot, 1);
+    cp(id_, b_ - 1, o - px, slot, 2);
+    if (!ZERO) {
+      cp(u, b_ + 1, o + px, slot, 3);
+      cp(sig, b_, o, slot, 4);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto shup = [](CS v) { return mkc<float>(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1)); };
+  auto shdn = [](CS v) {
+    return mkc<float>(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+  };
+#pragma unroll
+  for (int k = 0; k < PD; ++k) issue(k);
+  for (int it = 0; it < SEG + 4; ++it, ob += px) {
+    const int b = y0 - 2 + it;
+    issue(it + PD);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(PD) : "memory");
+    const float4 *sl = ring + (it % NST) * NA * 32 + lane;
+    auto split = [](float4 v, CS &p0, CS &p1) { p0 = mkc<float>(v.x, v.y); p1 = mkc<float>(v.z, v.w); };
+    CS fv[2], av[2], dv[2], sv[2] = {zs, zs};
+    split(sl[0], fv[0], fv[1]);
+    split(sl[32], av[0], av[1]);
+    split(sl[64], dv[0], dv[1]);
+    if (!ZERO) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) { ub1[q] = um1[q]; um1[q] = u0[q]; u0[q] = up1[q]; }
+      split(sl[96], up1[0], up1[1]);
+      split(sl[128], sv[0], sv[1]);
+    }
+    CD rb[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) rb[q] = ccast<D, float>(fv[q]);
+    if (!ZERO) {
+      using Q = TR;
+      using CQ = cplx<Q>;
+      // west / east neighbours of both nodes in rows b-1, b, b+1 (one shuffle pair per row)
+      CS wm[2], em[2], w0[2], e0[2], wp[2], ep[2];
+      wm[0] = shup(um1[1]); em[0] = um1[1]; wm[1] = um1[0]; em[1] = shdn(um1[0]);
+      w0[0] = shup(u0[1]);  e0[0] = u0[1];  w0[1] = u0[0];  e0[1] = shdn(u0[0]);
+      wp[0] = shup(up1[1]); ep[0] = up1[1]; wp[1] = up1[0]; ep[1] = shdn(up1[0]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const CQ uc = ccast<Q, float>(u0[q]);
+        const CQ un = ccast<Q, float>(um1[q]), us = ccast<Q, float>(up1[q]);
+        const CQ uw = ccast<Q, float>(w0[q]), ue = ccast<Q, float>(e0[q]);
+        const CQ sf = cadd<Q>(cadd<Q>(uw, ue), cadd<Q>(un, us));
+        CQ dlt = cadd<Q>(cadd<Q>(csub<Q>(uw, uc), csub<Q>(ue, uc)), cadd<Q>(csub<Q>(un, uc), csub<Q>(us, uc)));
+        CQ Lx = cscale<Q>(dlt, (Q)W::Lf);
+        if (W::Le != 0.0) {
+          const CQ d2 = cadd<Q>(cadd<Q>(csub<Q>(ccast<Q, float>(wm[q]), uc), csub<Q>(ccast<Q, float>(em[q]), uc)),
+                                cadd<Q>(csub<Q>(ccast<Q, float>(wp[q]), uc), csub<Q>(ccast<Q, float>(ep[q]), uc)));
+          Lx = cfmar<Q>(Lx, (Q)W::Le, d2);
+        }
+        Lx = cscale<Q>(Lx, (Q)ih2_d);
+        CQ Mx = cscale<Q>(uc, (Q)W::Mc);
+        if (W::Mf != 0.0) Mx = cfmar<Q>(Mx, (Q)W::Mf, sf);
+        CQ sq = ccast<Q, float>(sv[q]);
+        sq.y = fma(-(Q)alpha_d, sq.x, sq.y);
+        rb[q] = (xin[q] && yok(b)) ? ccast<D, Q>(csub<Q>(ccast<Q, float>(fv[q]), csub<Q>(Lx, cmul<Q>(sq, Mx)))) : z;
+      }
+    }
+    CD t0[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      r2[q] = r1[q]; r1[q] = r0[q]; r0[q] = rb[q];
+      a2[q] = a1[q]; a1[q] = a0[q]; a0[q] = av[q];
+      t0[q] = cmul<D>(rb[q], ccast<D, float>(av[q]));
+      h2[q] = h1[q]; h1[q] = h0[q];
+    }
+    h0[0] = cadd<D>(shfl_up1(t0[1]), t0[1]);
+    h0[1] = cadd<D>(t0[0], shfl_dn1(t0[0]));
+    CD yc[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const CD sdiag = cadd<D>(h2[q], h0[q]);
+      const CD num = mkc<D>(r1[q].x - e * sdiag.x, r1[q].y - e * sdiag.y);
+      yc[q] = (xin[q] && yok(b - 1)) ? cmul<D>(num, ccast<D, float>(dv[q])) : z;
+      c2[q] = c1[q]; c1[q] = yc[q];
+      g3[q] = g2[q]; g2[q] = g1[q];
+    }
+    g1[0] = cadd<D>(shfl_up1(yc[1]), yc[1]);
+    g1[1] = cadd<D>(yc[0], shfl_dn1(yc[0]));
+    const int yo = b - 2;
+    if (yo >= y0 && yo < y1 && out_lane && yok(yo)) {
+      CS o[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const CD syl = cadd<D>(g3[q], g1[q]);
+        const int xq = x0 + q + g.o[0];
+        const bool xm = xq - 1 >= 0, xp = xq + 1 < g.N[0];
+        const bool ym = yo - 1 >= ylo, yp = yo + 1 < yhi;
+        const int k = (int)(xm && ym) + (int)(xp && ym) + (int)(xm && yp) + (int)(xp && yp);
+        const D kd = (D)kRbCount[k];
+        const CD lv = cmul<D>(mkc<D>(kd * r2[q].x - e * syl.x, kd * r2[q].y - e * syl.y), ccast<D, float>(a2[q]));
+        const CD upd = cscale<D>(cadd<D>(c2[q], lv), w * (D)kRbInvCnt[k]);
+        o[q] = ccast<float, D>(ZERO ? upd : cadd<D>(ccast<D, float>(ub1[q]), upd));
+      }
+      float2 *dst = u_out + (ob - 2 * px);
+      if (outn[0] && outn[1]) *reinterpret_cast<float4 *>(dst) = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+      else if (outn[0]) dst[0] = o[0];
+    }
+  }
+}
+
 }  // namespace hmg
