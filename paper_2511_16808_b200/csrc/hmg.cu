@@ -709,6 +709,15 @@ template <typename T> struct Solver : SolverBase {
     }
     const C *cf = Lv.coef.template as<C>();
     const int64_t bs = Lv.geo.total;
+    if (opt.dim == 2 && nbat(l) == 1 && std::is_same<T, float>::value && (G % 2) == 0 && Lv.r <= 2 &&
+        std::getenv("HMG_NO_PAIR_ST") == nullptr) {   // two nodes per thread, 16-byte coefficient pairs
+      tag(f ? "stored_residual" : "stored_apply", l, kcount(opt.dim, Lv.r) * sizeof(C) * nn + (f ? 3 : 2) * sz * nn);
+      const dim3 block(32, 8), grid(((Lv.geo.n[0] + 1) / 2 + 31) / 32, (Lv.geo.n[1] + 7) / 8);
+      const float2 *c2 = reinterpret_cast<const float2 *>(cf);
+      if (Lv.r == 1) launch(k_stored_op2d_pair<1>, grid, block, 0, s, Lv.geo, c2, xx, ff, yy);
+      else launch(k_stored_op2d_pair<2>, grid, block, 0, s, Lv.geo, c2, xx, ff, yy);
+      return;
+    }
     over_batch(nbat(l), [&](auto NRc, int q0) {
       constexpr int NR = decltype(NRc)::value;
       const D *xq = xx + q0 * bs, *fq = ff ? ff + q0 * bs : nullptr;

@@ -183,4 +183,38 @@ __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__rest
   for (int r = 0; r < NR; ++r) y[r * bs + i] = f ? csub<T>(f[r * bs + i], acc[r]) : acc[r];
 }
 
+// 2D c64 variant of k_stored_op: one thread per PAIR of x-adjacent nodes (2p,
+// 2p+1): the fp32 coefficient planes load as aligned 16-byte pairs and the two
+// nodes share their x-window (2R + 2 loads per row instead of 2 (2R + 1)).  Same
+// per-node arithmetic and fma order as k_stored_op.
+template <int R>
+__global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *__restrict__ coef,
+                                                          const double2 *__restrict__ x,
+                                                          const double2 *__restrict__ f, double2 *__restrict__ y) {
+  using T = double;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ix = 2 * p;
+  if (ix >= g.n[0] || iy >= g.n[1]) return;
+  const int64_t i = g.idx(ix, iy, 0);
+  const bool two = ix + 1 < g.n[0];
+  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+  int k = 0;
+#pragma unroll
+  for (int oy = -R; oy <= R; ++oy) {
+    const double2 *row = x + i + (int64_t)oy * g.px;
+    double2 xw[2 * R + 2];
+#pragma unroll
+    for (int c = 0; c < 2 * R + 2; ++c) xw[c] = row[c - R];
+#pragma unroll
+    for (int ox = -R; ox <= R; ++ox, ++k) {
+      const float4 c2 = *reinterpret_cast<const float4 *>(coef + (int64_t)k * g.total + i);
+      a0 = cfma<T>(a0, mkc<T>(c2.x, c2.y), xw[ox + R]);
+      a1 = cfma<T>(a1, mkc<T>(c2.z, c2.w), xw[ox + R + 1]);
+    }
+  }
+  y[i] = f ? csub<T>(f[i], a0) : a0;
+  if (two) y[i + 1] = f ? csub<T>(f[i + 1], a1) : a1;
+}
+
 }  // namespace hmg
