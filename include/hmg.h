@@ -87,7 +87,10 @@ typedef struct {
   int dim;                    /* 2 or 3 */
   int64_t cells[3];           /* cells per axis, x first; each >= 4 and divisible by 2^(levels-1) */
   double h;                   /* uniform mesh size */
-  int levels;                 /* >= 2; level 0 = fine, levels-1 = coarsest (direct solve) */
+  int levels;                 /* >= 2; level 0 = fine, levels-1 = coarsest (direct solve).
+                                 1 = operator-only hierarchy: only the matrix-free fine operator
+                                 (apply / residual at level 0; cycle, smoother and solves return
+                                 HMG_EINVAL) -- no setup beyond sigma, for any grid that fits */
   int nu1, nu2;               /* pre/post smoothing steps (V(1,1): P:997) */
   int cycle;                  /* 0 = V-cycle, 1 = W-cycle (Alg. 2.1) */
   int fine_stencil;           /* HMG_COMPACT4 | HMG_FD2 */

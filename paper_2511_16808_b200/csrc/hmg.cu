@@ -326,6 +326,18 @@ template <typename T> struct Solver : SolverBase {
              gq.template as<double>(), sig.template as<C>(), sigd.template as<double2>());
       CK(cudaStreamSynchronize(s));
     }
+    if (L == 1) {   // operator-only hierarchy: the matrix-free fine operator, no cycle
+      if (comm && comm->size > 1) distribute(s);
+      lev[0].u.alloc(f0.total * sizeof(C), s);
+      lev[0].f.alloc(f0.total * sizeof(C), s);
+      lev[0].r_.alloc(f0.total * sizeof(C), s);
+      io.alloc((size_t)N0 * sizeof(C), s);
+      CK(cudaEventCreate(&ev0));
+      CK(cudaEventCreate(&ev1));
+      CK(cudaMallocHost((void **)&hpin, 4096 * sizeof(double)));
+      CK(cudaStreamSynchronize(s));
+      return;
+    }
     // level operators in fp64
     std::vector<DBuf> cd(L);
     lev[0].r = 1;
@@ -1039,13 +1051,18 @@ template <typename T> struct Solver : SolverBase {
     prolong_(l, lev[l + 1].u.p, lev[l].u.p, lev[l].u.p, s);
     unpack(l, lev[l].u.p, u, s);
   }
+  void need_cycle() const {
+    if (L < 2) throw HmgError(HMG_EINVAL, "operator-only hierarchy (levels = 1): no cycle, smoother or solve");
+  }
   void api_coarse(const void *r, void *e, cudaStream_t s) override {
+    need_cycle();
     Level &Lc = lev[L - 1];
     pack(L - 1, r, Lc.f.p, s);
     coarse_(Lc.f.p, Lc.u.p, s);
     unpack(L - 1, Lc.u.p, e, s);
   }
   void api_vcycle(const void *f, void *x, int zero, cudaStream_t s) override {
+    need_cycle();
     Level &Lv = lev[0];
     pack(0, f, Lv.f.p, s);
     if (!zero) pack(0, x, Lv.u.p, s);
@@ -1442,6 +1459,7 @@ template <typename T> struct Solver : SolverBase {
     if (m < 1 || m >= KRY_MAXV) throw HmgError(HMG_EINVAL, "restart must be in [1, 31]");
     if (!(tol > 0) || maxiter < 0) throw HmgError(HMG_EINVAL, "tol must be > 0 and maxiter >= 0");
     if (nr < 1) throw HmgError(HMG_EINVAL, "nrhs must be >= 1");
+    need_cycle();
     if (nr > 1 && comm && comm->size > 1) throw HmgError(HMG_EINVAL, "batched solves run on one rank");
     if (nr > 1 && host) throw HmgError(HMG_EINVAL, "batched solves take device buffers");
     ensure_ws(m, s);
@@ -1630,7 +1648,7 @@ static hmg_status build_impl(const hmg_options *o, const double *kappa, double o
   if (!o || !kappa || !gamma || !out) return fail(HMG_EINVAL, "null pointer");
   *out = nullptr;
   if (o->dim != 2 && o->dim != 3) return fail(HMG_EINVAL, "dim must be 2 or 3");
-  if (o->levels < 2 || o->levels > 16) return fail(HMG_EINVAL, "levels must be in [2, 16]");
+  if (o->levels < 1 || o->levels > 16) return fail(HMG_EINVAL, "levels must be in [1, 16] (1 = operator only)");
   if (!(o->h > 0)) return fail(HMG_EINVAL, "h must be > 0");
   if (!(omega > 0)) return fail(HMG_EINVAL, "omega must be > 0");
   if (!(alpha >= 0)) return fail(HMG_EINVAL, "shift alpha must be >= 0");

@@ -84,3 +84,43 @@ def test_config4_replica_deep():
     from paper_2511_16808_b200 import media
     p = media.config_problem(4, scale=8)
     check(*solve_both(p, 5, 0.5, 20, "c64", "element"), "c64")
+
+
+@pytest.mark.slow
+def test_config4_full_size_operator_sampled():
+    """BASELINE configs[4] at FULL size (769^2 x 385 nodes = 227.7 M unknowns, c64; SURVEY §8(d):
+    "at full size, compare apply_helmholtz ... on sampled rows").  The hierarchy is operator-only
+    (levels = 1: the full V-cycle setup does not fit one GPU).  H x and H_s x on
+    sampled rows against the oracle's own fine operator assembled on the 3^3 sub-box around each
+    row -- it holds every in-domain neighbour, so the truncation is the same as on the full grid."""
+    import torch
+    from paper_2511_16808_b200 import hmg, media
+    from oracle.operators import fine_operator, sigma_fields
+    p = media.config_problem(4)
+    alpha = 0.5
+    gh = hmg.Hierarchy(hmg.Options(dim=3, cells=p.cells, h=p.h, levels=1, smoother="element", dtype="c64"),
+                       p.kappa, p.omega, p.gamma, alpha)
+    nz, ny, nx = p.kappa.shape
+    g = torch.Generator().manual_seed(9)
+    xh = torch.complex(torch.randn(p.n, generator=g), torch.randn(p.n, generator=g))
+    xd = xh.cuda()
+    yd = torch.empty_like(xd)
+    sig, sig_s = sigma_fields(p.kappa, p.gamma, p.omega, alpha)
+    sig, sig_s = np.asarray(sig).reshape(nz, ny, nx), np.asarray(sig_s).reshape(nz, ny, nx)
+    xs = xh.numpy().reshape(nz, ny, nx)
+    rng = np.random.default_rng(4)
+    pts = [(0, 0, 0), (nz - 1, ny - 1, nx - 1), (0, ny // 2, nx // 2), (nz // 2, 0, nx - 1)]
+    pts += [tuple(int(v) for v in (rng.integers(0, nz), rng.integers(0, ny), rng.integers(0, nx))) for _ in range(1500)]
+    for shifted, sgm in ((False, sig), (True, sig_s)):
+        gh.apply_helmholtz(xd, yd, level=0, shifted=shifted)
+        y = yd.cpu().numpy().reshape(nz, ny, nx)
+        for (iz, iy, ix) in pts:
+            zs, ys, xs_ = [slice(max(0, i - 1), min(n, i + 2)) for i, n in ((iz, nz), (iy, ny), (ix, nx))]
+            sub_nodes = (xs_.stop - xs_.start, ys.stop - ys.start, zs.stop - zs.start)
+            A = fine_operator(sub_nodes, p.h, sgm[zs, ys, xs_].ravel())
+            xsub = xs[zs, ys, xs_].ravel().astype(np.complex128)
+            row = ((iz - zs.start) * sub_nodes[1] + (iy - ys.start)) * sub_nodes[0] + (ix - xs_.start)
+            want = A[row] @ xsub
+            scale = abs(A[row]) @ np.abs(xsub)
+            # fp32 storage of x and sigma, fp64 arithmetic: well inside 1e-5 of sum |terms|
+            assert abs(y[iz, iy, ix] - want[0]) <= 1e-5 * scale[0], (shifted, iz, iy, ix)

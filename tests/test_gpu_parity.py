@@ -365,3 +365,25 @@ def test_errors():
         hmg.Hierarchy(hmg.Options(dim=2, cells=(8, 8), h=h, levels=2, smoother="jacobi", fine_stencil="fd2",
                                   damping=[0.8]), np.ones(81), 16.0, np.zeros(81), 0.0)
     assert e.value.status == hmg.ESINGULAR_PATCH and "level 0" in str(e.value)
+
+
+def test_operator_only_hierarchy():
+    """levels = 1: the matrix-free fine operator alone (no setup beyond sigma); apply and
+    residual match the oracle, cycle / solve calls are rejected with HMG_EINVAL."""
+    import torch
+    from paper_2511_16808_b200 import hmg
+    from oracle.operators import fine_operator, sigma_fields
+    p = problem(2, (40, 24))
+    gh = hmg.Hierarchy(hmg.Options(dim=2, cells=p.cells, h=p.h, levels=1, damping=[0.83]), p.kappa, p.omega,
+                       p.gamma, 0.3)
+    sig, sig_s = sigma_fields(p.kappa, p.gamma, p.omega, 0.3)
+    nodes = tuple(c + 1 for c in p.cells)
+    x = _rand(p.n, 3)
+    y = to_dev(np.zeros(p.n))
+    for shifted, sg in ((False, sig), (True, sig_s)):
+        gh.apply_helmholtz(to_dev(x), y, level=0, shifted=shifted)
+        assert rel_err(to_host(y), fine_operator(nodes, p.h, sg) @ x) <= TOL_OP["c128"]
+    with pytest.raises(hmg.HmgError):
+        gh.vcycle(to_dev(x), y)
+    with pytest.raises(hmg.HmgError):
+        gh.fgmres_solve(to_dev(x), y)
