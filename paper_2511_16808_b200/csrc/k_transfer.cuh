@@ -50,61 +50,7 @@ __global__ void __launch_bounds__(256) k_restrict(Geo gf, Geo gc, const cplx<TI>
   fc[ic] = ccast<TO, T>(acc);
 }
 
-// u[i] += sum_J P[i, J] e[J]     (fine-node parallel)
-template <int PR>
-__device__ __forceinline__ int prolong_taps(int i, int *J, double *w) {
-  // returns number of taps along one axis for fine coordinate i
-  if ((i & 1) == 0) {
-    const int c = i >> 1;
-    if (PR == 2) {
-      J[0] = c - 1; w[0] = 0.125;
-      J[1] = c;     w[1] = 0.75;
-      J[2] = c + 1; w[2] = 0.125;
-      return 3;
-    }
-    J[0] = c; w[0] = 1.0;
-    return 1;
-  }
-  const int c = (i - 1) >> 1;
-  J[0] = c;     w[0] = 0.5;
-  J[1] = c + 1; w[1] = 0.5;
-  return 2;
-}
-
-// u_out = u + P e (u_out may equal u: each node reads and writes only itself)
-template <typename TE, typename TU, int DIM, int PR>
-__global__ void __launch_bounds__(256) k_prolong_add(Geo gf, Geo gc, const cplx<TE> *__restrict__ e,
-                                                     const cplx<TU> *u, cplx<TU> *u_out) {
-  using T = double;
-  HMG_NODE_IDX(gf, ix, iy, iz);
-  int Jx[3], Jy[3], Jz[3];
-  double wx[3], wy[3], wz[3];
-  // taps from GLOBAL fine coordinates (parity decides), then coarse-local indices
-  const int nx = prolong_taps<PR>(ix + gf.o[0], Jx, wx);
-  const int ny = prolong_taps<PR>(iy + gf.o[1], Jy, wy);
-  int nz = 1;
-  Jz[0] = 0; wz[0] = 1.0;
-  if (DIM == 3) nz = prolong_taps<PR>(iz + gf.o[2], Jz, wz);
-  for (int a = 0; a < nx; ++a) Jx[a] -= gc.o[0];
-  for (int b = 0; b < ny; ++b) Jy[b] -= gc.o[1];
-  if (DIM == 3)
-    for (int c = 0; c < nz; ++c) Jz[c] -= gc.o[2];
-  cplx<T> acc = mkc<T>(0, 0);
-  for (int c = 0; c < nz; ++c) {
-    cplx<T> accy = mkc<T>(0, 0);
-    for (int b = 0; b < ny; ++b) {
-      cplx<T> accx = mkc<T>(0, 0);
-      const int64_t row = gc.base + (int64_t)Jz[c] * gc.pxy + (int64_t)Jy[b] * gc.px;
-      for (int a = 0; a < nx; ++a) accx = cfmar<T>(accx, (T)wx[a], ccast<T, TE>(e[row + Jx[a]]));
-      accy = cfmar<T>(accy, (T)wy[b], accx);
-    }
-    acc = cfmar<T>(acc, (T)wz[c], accy);
-  }
-  const int64_t i = gf.idx(ix, iy, iz);
-  u_out[i] = ccast<TU, T>(cadd<T>(ccast<T, TU>(u[i]), acc));
-}
-
-// Same operation, coarse-node parallel: the thread of coarse node J writes
+// Prolongation + correction  u_out = u + P e  (Alg. 2.1 step 4), coarse-node parallel: the thread of coarse node J writes
 // the 2^d fine nodes 2J + {0,1}^d (global parity), loading its 3^d coarse
 // neighbourhood once (instead of up to 3^d loads per fine node).  Fine nodes
 // outside this rank's rows / the domain are skipped.  u_out may equal u.
