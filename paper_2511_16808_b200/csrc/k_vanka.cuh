@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
 // loop and predicate logic) is shared by the two nodes.
 constexpr int RB2_STRIP = 56;
 
-template <int KIND, bool ZERO, int SEG, typename TR, int MINB, int PD>
+template <int KIND, bool ZERO, int SEG, typename TR, int MINB, int PD, int UNR = 1>
 __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *__restrict__ sig,
                                                            const float2 *__restrict__ ia_,
                                                            const float2 *__restrict__ id_, double alpha_d,
@@ -477,6 +477,8 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
   };
 #pragma unroll
   for (int k = 0; k < PD; ++k) issue(k);
+  static_assert((SEG + 4) % UNR == 0, "unroll must divide the trip count");
+#pragma unroll UNR
   for (int it = 0; it < SEG + 4; ++it, ob += px) {
     const int b = y0 - 2 + it;
     issue(it + PD);
