@@ -52,8 +52,8 @@ def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+        return float(d["hbm_gbs"]), "of measured (MEASURED_PEAKS.json hbm_gbs: STREAM-style copy, the only HBM figure)"
+    return 6650.0, "of fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 class ClockSampler:
