@@ -1,10 +1,11 @@
-"""Oracle (CPU, SciPy, complex128) timed on the GPU box's host, beside the GPU numbers
+"""(Test infrastructure: lives under tests/ because it runs the oracle.)
+Oracle (CPU, SciPy, complex128) timed on the GPU box's host, beside the GPU numbers
 (SURVEY §8(d) "Oracle timing beside it").  Setup and solve are reported separately.
 Small cases are solved in full; for the large ones the first restart cycle (m iterations)
 is timed and the full solve is extrapolated with the GPU's iteration count for the same
 configuration (labelled "extrapolated").
 
-    python scripts/oracle_timing.py [--out profiles/r01_oracle_timing.jsonl] [--budget-s 900]
+    python tests/tools/oracle_timing.py [--out profiles/r01_oracle_timing.jsonl] [--budget-s 900]
 """
 import argparse
 import json
@@ -13,7 +14,7 @@ import platform
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 RB2 = [0.83, 0.5, 0.4, 0.65]
