@@ -267,6 +267,9 @@ template <typename T> struct Solver : SolverBase {
   // buffers, so one capture serves every call); single-rank runs only
   std::map<int, cudaGraphExec_t> cgraphs;   // coarse-cycle graph per batch width
   std::map<int, long long> cgraph_kernels_nr;
+  // whole zero-guess V-cycles (level 0 included) per (f, u) buffer pair: FGMRES feeds the
+  // same m pairs (V_j, Z_j) every restart, so each pair's graph is captured once
+  std::map<std::pair<const void *, void *>, std::pair<cudaGraphExec_t, long long>> fgraphs;
   // multi-RHS batches: levels >= 1 hold nrb right-hand sides at a stride of one
   // padded box (capacity nrb_cap); the fine level runs per right-hand side
   int nrb = 1, nrb_cap = 1;
@@ -278,6 +281,7 @@ template <typename T> struct Solver : SolverBase {
 
   ~Solver() override {
     for (auto &kv : cgraphs) cudaGraphExecDestroy(kv.second);
+    for (auto &kv : fgraphs) cudaGraphExecDestroy(kv.second.first);
     if (gev_in) cudaEventDestroy(gev_in);
     if (gev_out) cudaEventDestroy(gev_out);
     if (gstream) cudaStreamDestroy(gstream);
@@ -967,6 +971,37 @@ template <typename T> struct Solver : SolverBase {
     CK(cudaStreamWaitEvent(s, gev_out, 0));
   }
 
+  // u <- MG_0(f, 0) as ONE graph launch (level 0 included), captured per (f, u) pair
+  void full_cycle_graph(const void *f, void *u, cudaStream_t s) {
+    if (!gstream) {
+      CK(cudaStreamCreateWithFlags(&gstream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&gev_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&gev_out, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(gev_in, s));
+    CK(cudaStreamWaitEvent(gstream, gev_in, 0));
+    const auto key = std::make_pair(f, u);
+    auto it = fgraphs.find(key);
+    if (it == fgraphs.end()) {
+      const long long k0 = launch_count_now();
+      cudaGraph_t gr;
+      CK(cudaStreamBeginCapture(gstream, cudaStreamCaptureModeThreadLocal));
+      cycle(0, f, u, 1, gstream, true);
+      CK(cudaStreamEndCapture(gstream, &gr));
+      cudaGraphExec_t ex;
+      CK(cudaGraphInstantiate(&ex, gr, 0));
+      CK(cudaGraphDestroy(gr));
+      const long long nk = launch_count_now() - k0;
+      add_launches(-nk);                                 // captured, not launched
+      it = fgraphs.emplace(key, std::make_pair(ex, nk)).first;
+    }
+    CK(cudaGraphLaunch(it->second.first, gstream));
+    add_launches(it->second.second);
+    CK(cudaEventRecord(gev_out, gstream));
+    CK(cudaStreamWaitEvent(s, gev_out, 0));
+  }
+  bool full_graph_ok() const { return graphs_ok() && L > 1 && std::getenv("HMG_NO_FULL_GRAPH") == nullptr; }
+
   // Alg. 2.1, recursive; u <- MG_l(f, u)
   void cycle(int l, const void *f, void *u, int zero, cudaStream_t s, bool capturing = false) {
     if (l == 1 && zero && !capturing && L > 2 && f == lev[1].f.p && u == lev[1].u.p && graphs_ok()) {
@@ -1224,7 +1259,10 @@ template <typename T> struct Solver : SolverBase {
   void cycle_batch(const std::vector<const C *> &f, const std::vector<C *> &u, cudaStream_t s) {
     const int na = (int)f.size();
     if (na == 1 || L < 2) {
-      for (int k = 0; k < na; ++k) cycle(0, f[k], u[k], 1, s);
+      for (int k = 0; k < na; ++k) {
+        if (full_graph_ok()) full_cycle_graph(f[k], u[k], s);
+        else cycle(0, f[k], u[k], 1, s);
+      }
       return;
     }
     ensure_batch(na, s);
@@ -1266,6 +1304,8 @@ template <typename T> struct Solver : SolverBase {
     }
     for (auto &kv : cgraphs) cudaGraphExecDestroy(kv.second);
     cgraphs.clear();
+    for (auto &kv : fgraphs) cudaGraphExecDestroy(kv.second.first);
+    fgraphs.clear();
     nrb_cap = nr;
   }
 
