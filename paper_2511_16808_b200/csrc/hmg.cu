@@ -278,6 +278,7 @@ template <typename T> struct Solver : SolverBase {
   int nblk = 0;
   double *hpin = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_dots = nullptr;   // the Arnoldi dots have reached the host (pipelined FGMRES)
 
   ~Solver() override {
     for (auto &kv : cgraphs) cudaGraphExecDestroy(kv.second);
@@ -288,6 +289,7 @@ template <typename T> struct Solver : SolverBase {
     if (hpin) cudaFreeHost(hpin);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_dots) cudaEventDestroy(ev_dots);
   }
 
   const Geo &g0() const { return lev[0].geo; }
@@ -338,6 +340,7 @@ template <typename T> struct Solver : SolverBase {
       io.alloc((size_t)N0 * sizeof(C), s);
       CK(cudaEventCreate(&ev0));
       CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreateWithFlags(&ev_dots, cudaEventDisableTiming));
       CK(cudaMallocHost((void **)&hpin, 4096 * sizeof(double)));
       CK(cudaStreamSynchronize(s));
       return;
@@ -467,6 +470,7 @@ template <typename T> struct Solver : SolverBase {
     io.alloc((size_t)N0 * sizeof(C), s);
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreateWithFlags(&ev_dots, cudaEventDisableTiming));
     CK(cudaMallocHost((void **)&hpin, 4096 * sizeof(double)));
     CK(cudaStreamSynchronize(s));
   }
@@ -1233,6 +1237,7 @@ template <typename T> struct Solver : SolverBase {
     std::vector<double> nbeta, hist;
     int m = 0, j = 0, its = 0, restarts = 0;
     bool active = true, converged = false, start = true, have_res = false, failed = false;
+    bool pre = false;   // this step's cycle and matvec were already enqueued (speculatively)
     double qn = 0, true_rel = 1, est = 1;
     cd &Hs(int i, int k) { return H[(size_t)i * m + k]; }
   };
@@ -1336,12 +1341,13 @@ template <typename T> struct Solver : SolverBase {
   // W_j = nb[j] v_j with nb[j] = ||W_j|| (nb[0] = 1); the cycle and the matvec
   // run on W_j, so d_i = W_i^H (H M W_j) = nb[i] nb[j] h_ij, the AXPY removes
   // (d_i / nb[i]^2) W_i, and W_{j+1} = nb[j] w_perp needs no scaling pass.
-  void fgmres_step(RhsState &r, double tol, int maxiter, cudaStream_t s) {
+  void fgmres_step(RhsState &r, double tol, int maxiter, cudaStream_t s, bool speculate = false) {
     const int j = r.j, m = r.m;
     double2 *dr = dres.template as<double2>();
     double *ib2h = hpin + 512, *ib2d = reinterpret_cast<double *>(dr + 160);
     C *w = Vp(j + 1);
-    matvec(Zp(j), w, s);                              // w' = H z'_j (fp64 arithmetic)
+    if (!r.pre) matvec(Zp(j), w, s);                  // w' = H z'_j (fp64 arithmetic)
+    r.pre = false;
     const int nv = j + 1;
     for (int i = 0; i <= j; ++i) ib2h[i] = 1.0 / (r.nbeta[i] * r.nbeta[i]);
     CK(cudaMemcpyAsync(ib2d, ib2h, nv * sizeof(double), cudaMemcpyHostToDevice, s));
@@ -1352,12 +1358,25 @@ template <typename T> struct Solver : SolverBase {
     mdot<T, T>(V.template as<C>(), nv, w, dr, s, true);            // d = W^H w', ||w'||^2
     maxpy<T, T>(V.template as<C>(), nv, dr, -1.0, w, dr + 64, s, ib2d);   // w'' = w' - W diag(1/nb^2) d
     CK(cudaMemcpyAsync(hpin, dr, 65 * sizeof(double2), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    // Pipelining (single right-hand side): W_{j+1} is complete on the device, so the next
+    // preconditioner application and matvec are enqueued BEFORE the host waits for the dots;
+    // the Givens update overlaps the next V-cycle.  If W_{j+1} changes afterwards (second
+    // Gram-Schmidt pass, range rescaling) or the cycle ends here, the speculative work is
+    // discarded / redone -- every iterate stays that of the unpipelined solve.
+    const bool spec = speculate && j + 1 < m && r.its + 1 < maxiter;
+    CK(cudaEventRecord(ev_dots, s));
+    if (spec) {
+      cycle_batch({Vp(j + 1)}, {Zp(j + 1)}, s);
+      matvec(Zp(j + 1), Vp(j + 2), s);
+    }
+    CK(cudaEventSynchronize(ev_dots));
+    bool spec_ok = spec;
     const double2 *hh = reinterpret_cast<const double2 *>(hpin);
     for (int i = 0; i <= j; ++i) r.Hs(i, j) = cd(hh[i].x, hh[i].y) / (r.nbeta[i] * r.nbeta[j]);
     double hn2 = hh[64].x;
     if (!(hn2 >= kReorthEta2 * hh[nv].x)) {
       ++reorth;
+      spec_ok = false;                                // W_{j+1} changes: redo the next cycle
       mdot<T, T>(V.template as<C>(), nv, w, dr + 32, s);
       maxpy<T, T>(V.template as<C>(), nv, dr + 32, -1.0, w, dr + 64, s, ib2d);
       CK(cudaMemcpyAsync(hpin + 64, dr + 32, 33 * sizeof(double2), cudaMemcpyDeviceToHost, s));
@@ -1377,6 +1396,7 @@ template <typename T> struct Solver : SolverBase {
     if (!breakdown && (wn < 1e-25 || wn > 1e25)) {   // keep the stored basis in range (rare)
       scale<T, T>(w, w, 1.0 / wn, s);
       r.nbeta[j + 1] = 1.0;
+      spec_ok = false;                                // W_{j+1} changes: redo the next cycle
     }
     for (int i = 0; i < j; ++i) {                    // previous Givens rotations
       const cd t = r.cs[i] * r.Hs(i, j) + r.sn[i] * r.Hs(i + 1, j);
@@ -1398,6 +1418,7 @@ template <typename T> struct Solver : SolverBase {
     const bool stop = r.est < tol || breakdown || r.its >= maxiter;
     if (!stop && j + 1 < m) {
       r.j = j + 1;
+      r.pre = spec_ok;                                // its cycle and matvec are already enqueued
       return;
     }
     // end of a restart cycle: x += Z y (fp64), then the fp64 true residual
@@ -1466,10 +1487,11 @@ template <typename T> struct Solver : SolverBase {
         fv.push_back(r->V.template as<C>() + (size_t)r->j * g0().total);
         uv.push_back(r->Z.template as<C>() + (size_t)r->j * g0().total);
       }
-      cycle_batch(fv, uv, s);
+      const bool single = act.size() == 1 && std::getenv("HMG_NO_PIPELINE") == nullptr;
+      if (!(single && act[0]->pre)) cycle_batch(fv, uv, s);   // (already enqueued when pipelined)
       for (RhsState *r : act) {
         bind(*r);
-        fgmres_step(*r, tol, maxiter, s);
+        fgmres_step(*r, tol, maxiter, s, single);
         bind(*r);
       }
     }
