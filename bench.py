@@ -357,7 +357,7 @@ def main():
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--maxiter", type=int, default=4000)
     ap.add_argument("--cpu-n", type=int, default=512)
-    ap.add_argument("--cpu-iters", type=int, default=40)
+    ap.add_argument("--cpu-iters", type=int, default=120, help="oracle FGMRES iterations per CPU sample (~10 s at --cpu-n 512)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nrhs", type=int, default=4, help="batch size of the multi-RHS line (<= 1: skip)")
     args = ap.parse_args()
