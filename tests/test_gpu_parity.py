@@ -387,3 +387,24 @@ def test_operator_only_hierarchy():
         gh.vcycle(to_dev(x), y)
     with pytest.raises(hmg.HmgError):
         gh.fgmres_solve(to_dev(x), y)
+
+
+@pytest.mark.parametrize("dtype,restart,maxiter", [("c64", 10, 500), ("c128", 5, 7), ("c64", 4, 13)])
+def test_pipelined_fgmres_identical(monkeypatch, dtype, restart, maxiter):
+    """The pipelined FGMRES (next V-cycle enqueued before the host reads the Arnoldi dots; redone
+    on reorthogonalisation, dropped at restart ends and at maxiter) returns exactly the iterates of
+    the unpipelined solve, including runs that stop at maxiter inside a restart cycle."""
+    import torch
+    from paper_2511_16808_b200 import hmg
+    p = media.config_problem(0)
+    gh = hmg.Hierarchy(hmg.Options(dim=2, cells=p.cells, h=p.h, levels=4, damping=[0.83, 0.5, 0.4, 0.65],
+                                   dtype=dtype), p.kappa, p.omega, p.gamma, 0.15)
+    cdt = torch.complex64 if dtype == "c64" else torch.complex128
+    q = torch.from_numpy(p.q.ravel()).to(cdt).cuda()
+    x1, x2 = torch.zeros_like(q), torch.zeros_like(q)
+    r1 = gh.fgmres_solve(q, x1, restart=restart, tol=1e-6, maxiter=maxiter)
+    monkeypatch.setenv("HMG_NO_PIPELINE", "1")
+    r2 = gh.fgmres_solve(q, x2, restart=restart, tol=1e-6, maxiter=maxiter)
+    assert r1.iterations == r2.iterations and r1.history == r2.history
+    assert r1.converged == r2.converged and r1.relres_true == r2.relres_true
+    assert torch.equal(x1, x2)
