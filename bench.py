@@ -239,6 +239,10 @@ def run_ours(args):
                    "parallelism": (f"slab-partitioned over {ws} GPUs (y-slabs, NCCL halos + allreduce, "
                                    f"coarse levels replicated)") if ws > 1 else "single GPU",
                    "l2": "inputs larger than L2 (every vector >= 134 MB at N=4096; no flush needed)",
+                   "precision": ("c64: fine-level vectors, Krylov basis and all coefficients stored in fp32 complex; "
+                                 "coarse-level vectors, FGMRES iterate / RHS / restart residual in fp64; arithmetic "
+                                 "fp64 except the fine post-sweep residual (fp32, difference form) -- DESIGN.md 4.1")
+                   if args.dtype == "c64" else "c128: fp64 complex storage and arithmetic",
                    "setup_s": round(setup_s, 2)},
         "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
         "roofline": roofline,
