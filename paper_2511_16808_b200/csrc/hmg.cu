@@ -763,7 +763,12 @@ template <typename T> struct Solver : SolverBase {
     auto nl = node_launch(gc);
     using BI = decltype(r->x);
     tag("restrict", l, (double)sizeof(TI) * F.geo.nodes() + (double)sizeof(D) * gc.nodes());
-    if (opt.dim == 2) {
+    static const bool nopr = std::getenv("HMG_NO_PAIR_RS") != nullptr;
+    if (l == 0 && F.rR == 2 && std::is_same<T, float>::value && (G % 2) == 0 && (F.geo.base % 2) == 0 && !nopr) {
+      const float2 *r2 = reinterpret_cast<const float2 *>(r);   // c64 fine level: 16-byte pair loads
+      if (opt.dim == 2) launch(k_restrict_pair<2>, nl.grid, nl.block, 0, s, F.geo, gc, r2, fc);
+      else launch(k_restrict_pair<3>, nl.grid, nl.block, 0, s, F.geo, gc, r2, fc);
+    } else if (opt.dim == 2) {
       if (F.rR == 1) launch(k_restrict<BI, double, 2, 1>, nl.grid, nl.block, 0, s, F.geo, gc, r, fc);
       else launch(k_restrict<BI, double, 2, 2>, nl.grid, nl.block, 0, s, F.geo, gc, r, fc);
     } else {
