@@ -185,8 +185,10 @@ def test_smooth(dim, cells, smoother, dtype):
         fh, uh = to_host(f), to_host(u)
         gh.smooth(f, u, level=l)
         want = smooth(oh, l, fh, uh)
-        tol = TOL_OP[dtype] * (10 if dtype == "c128" else 1)
-        assert rel_err(to_host(u), want) <= tol, f"level {l}"
+        # c128: the single-operator bar (north_star 1e-12).  The step applies the fp64 patch
+        # inverses, so its rounding carries their condition numbers (measured here:
+        # DESIGN.md §3); the bar holds with them.
+        assert rel_err(to_host(u), want) <= TOL_OP[dtype], f"level {l}"
 
 
 def test_fd2_rb_is_jacobi():
@@ -281,6 +283,64 @@ def test_fgmres_config0(dtype):
     ho = np.array(info["history"])
     m = min(len(h), len(ho), 20)
     assert np.allclose(h[:m], ho[:m], rtol=1e-6 if dtype == "c128" else 1e-2)
+
+
+def test_fgmres_config0_rediscretize():
+    """SURVEY §8(f)3 / reading A13 end to end: config 0 with REDISCRETIZE coarse
+    operators (FW-averaged w^2k^2, g/w and the fine stencil at 2h) instead of
+    Galerkin.  FGMRES(10) iterations within +-1 of the oracle's (survey T10: 80-95 against
+    Galerkin's 30, the paper's reason for Galerkin), solution to 1e-5."""
+    p = media.config_problem(0)
+    from paper_2511_16808_b200 import hmg
+    from oracle.hierarchy import Options as OOptions, build_hierarchy
+    from oracle.fgmres import fgmres_solve
+    from oracle.cycle import vcycle
+    import torch
+    damping = [0.83, 0.5, 0.4, 0.65]
+    gh = hmg.Hierarchy(hmg.Options(dim=2, cells=p.cells, h=p.h, levels=4, coarse_op="rediscretize",
+                                   damping=damping, dtype="c128"), p.kappa, p.omega, p.gamma, 0.15)
+    oh = build_hierarchy(OOptions(dim=2, cells=p.cells, h=p.h, levels=4, coarse_op="rediscretize",
+                                  damping=damping), p.kappa, p.omega, p.gamma, 0.15)
+    xo, info = fgmres_solve(oh.H, p.q.ravel(), lambda v: vcycle(oh, v), restart=10, tol=1e-6, maxiter=1000)
+    q = to_dev(p.q)
+    x = torch.zeros_like(q)
+    rep = gh.fgmres_solve(q, x, restart=10, tol=1e-6, maxiter=1000)
+    assert info["converged"] and rep.converged and rep.relres_true <= 1e-6
+    assert abs(rep.iterations - info["iterations"]) <= 1, (rep.iterations, info["iterations"])
+    assert info["iterations"] > 45      # clearly worse than Galerkin's 30 (P:323-324)
+    assert rel_err(to_host(x), xo) <= 1e-5
+    # one V-cycle of the REDISCRETIZE hierarchy at the cycle bar
+    z = torch.zeros_like(q)
+    gh.vcycle(q, z)
+    assert rel_err(to_host(z), vcycle(oh, p.q.ravel())) <= TOL_CYCLE["c128"]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_vcycle_sponge_per_node(dtype):
+    """Per-node relative parity inside the absorbing layer (a max-abs
+    bar normalised by the global maximum cannot see errors on small entries).  Config 0,
+    one V-cycle of the point source: every node of the 16-node sponge band within
+    1e-9 (c128) / 1e-3 (c64) of the oracle relative to its own magnitude."""
+    p, gh, _, _ = _config0(dtype)
+    from oracle.hierarchy import Options as OOptions, build_hierarchy
+    from oracle.cycle import vcycle
+    import torch
+    oh = build_hierarchy(OOptions(dim=2, cells=p.cells, h=p.h, levels=4, damping=[0.83, 0.5, 0.4, 0.65]),
+                         p.kappa, p.omega, p.gamma, 0.15)
+    q = to_dev(p.q, dtype)
+    z = torch.zeros_like(q)
+    gh.vcycle(q, z)
+    zo = vcycle(oh, to_host(q))
+    zg = to_host(z)
+    n = 129
+    iy, ix = np.divmod(np.arange(n * n), n)
+    d = np.minimum(np.minimum(ix, n - 1 - ix), np.minimum(iy, n - 1 - iy))
+    band = d < 16
+    mag = np.abs(zo[band])
+    err = np.abs(zg[band] - zo[band])
+    floor = 1e-14 * np.abs(zo).max()
+    worst = float((err / np.maximum(mag, floor)).max())
+    assert worst <= (1e-9 if dtype == "c128" else 1e-3), (worst, float(mag.min() / np.abs(zo).max()))
 
 
 def test_fgmres_config0_plain_cslp():

@@ -72,6 +72,85 @@ def test_stencil_symbol_3d(theta):
     np.testing.assert_allclose((H @ v)[m], sym * v[m], rtol=1e-12)
 
 
+@pytest.mark.parametrize("dim,theta", [(2, (0.3, -1.1)), (2, (np.pi, 2.2)), (3, (0.3, -1.1, 0.5)),
+                                       (3, (2.0, 0.7, -2.9))])
+def test_fd2_stencil_symbol(dim, theta):
+    """Option FD2 (north_star "5-/7-point"; reading A12): the standard
+    second-order operator -Delta_h - sigma acts on a plane wave e^{i theta.x} as the
+    textbook symbol (2d - 2 sum_k cos theta_k)/h^2 - sigma at every interior node.
+    A wrong centre weight (e.g. 4/h^2 in 3D) or a stray M fails it."""
+    h, sigma = 1 / 16, 400.0 - 50.0j
+    nodes = (17,) * dim
+    H = fine_operator(nodes, h, np.full(17 ** dim, sigma), FD2)
+    v = plane_wave(nodes, theta)
+    sym = (2 * dim - 2 * np.cos(theta).sum()) / h ** 2 - sigma
+    m = interior_mask(nodes, 1)
+    np.testing.assert_allclose((H @ v)[m], sym * v[m], rtol=1e-12)
+    # 2d + 1 nonzeros in an interior row, 2d + 1 - (#boundary faces) at the boundary
+    nnz = np.diff(H.indptr)
+    assert nnz[m].min() == nnz[m].max() == 2 * dim + 1
+    assert nnz[0] == dim + 1
+
+
+def test_rediscretize_fw_average_pins():
+    """REDISCRETIZE coarsening of (w^2 k^2, g/w) (reading A13): full-weighting
+    average = truncated linear restriction [1 2 1]/4 per axis, row-normalised.
+    Pins: constants are preserved at EVERY coarse node; linear fields at interior
+    coarse nodes; the quadratic x^2 maps to x^2 + 1/2 (in fine-node units) at interior
+    nodes -- a closed form that fixes the weights (e.g. [1 1 1]/3 would give x^2 + 2/3);
+    at the boundary node the truncated row is (2 f_0 + f_1)/3 per axis."""
+    from oracle.hierarchy import _fw_average
+    for nodes in ((17, 9), (9, 9, 5)):
+        c = node_coords(nodes)
+        N = int(np.prod(nodes))
+        cn = tuple((n - 1) // 2 + 1 for n in nodes)
+        cc = node_coords(cn)
+        np.testing.assert_allclose(_fw_average(nodes, np.full(N, 3.25)), 3.25, rtol=1e-15)
+        inner = np.ones(int(np.prod(cn)), bool)
+        for a, n in enumerate(cn):
+            inner &= (cc[a] >= 1) & (cc[a] <= n - 2)
+        lin = 1.5 + 0.25 * c[0] - 0.75 * c[-1]
+        np.testing.assert_allclose(_fw_average(nodes, lin)[inner], (1.5 + 0.5 * cc[0] - 1.5 * cc[-1])[inner],
+                                   rtol=1e-14)
+        quad = c[0].astype(float) ** 2
+        np.testing.assert_allclose(_fw_average(nodes, quad)[inner], ((2 * cc[0]) ** 2 + 0.5)[inner], rtol=1e-14)
+    # 1D-separable boundary row in 2D: coarse node (0, 0) sees fine (0..1) x (0..1) with weights (2, 1) x (2, 1) / 9
+    nodes = (9, 9)
+    f = np.random.default_rng(3).random(81)
+    F = f.reshape(9, 9)   # [y, x]
+    want = (4 * F[0, 0] + 2 * F[0, 1] + 2 * F[1, 0] + F[1, 1]) / 9.0
+    assert abs(_fw_average(nodes, f)[0] - want) < 1e-15
+
+
+@pytest.mark.parametrize("sigma_h2", [0.0, 2.0 - 0.5j, 0.6 - 0.05j])
+def test_mu_loc_jacobi_closed_form(sigma_h2):
+    """lfa.mu_loc (Def. 2.1; high-frequency set and midpoint sampling P:641)
+    against a closed form for the 1x1 patch (damped Jacobi): with c_k = cos t_k,
+    S~ = 1 - w H~/a is bilinear in (c1, c2), |S~| is convex in each c_k separately, and
+    T_high in cosine space is the L-shaped set {c1 <= 0 or c2 <= 0} of [-1, 1]^2, so
+    sup |S~| is attained at one of the corners of its two rectangles.  For the Laplacian
+    (sigma = 0) this is the textbook max(|1 - 0.6 w|, |1 - 1.6 w|), minimal (5/11) at
+    w = 10/11.  The sampled maximum never exceeds the sup and approaches it as the
+    grid refines."""
+    h = 1.0 / 64
+    sigma = sigma_h2 / h ** 2
+    a = 10 / (3 * h * h) - 2 * sigma / 3
+    b = -2 / (3 * h * h) - sigma / 12
+    c = -1 / (6 * h * h)
+    corners = [(-1, -1), (-1, 1), (0, -1), (0, 1), (-1, 0), (1, -1), (1, 0)]
+    for w in (0.6, 0.89, 10 / 11):
+        sup = max(abs(1 - w * (a + 2 * b * (c1 + c2) + 4 * c * c1 * c2) / a) for c1, c2 in corners)
+        m256 = lfa.mu_loc("jacobi", sigma, h, w, n=256)
+        m1024 = lfa.mu_loc("jacobi", sigma, h, w, n=1024)
+        assert m256 <= sup + 1e-12 and m1024 <= sup + 1e-12
+        # the sampled sup converges at O(step): the 1024-grid gap is small and shrinks
+        assert sup - m1024 <= 5e-3 and sup - m1024 <= 0.6 * (sup - m256) + 1e-9
+        if sigma_h2 == 0.0:
+            assert abs(sup - max(abs(1 - 0.6 * w), abs(1 - 1.6 * w))) < 1e-12
+    if sigma_h2 == 0.0:
+        assert abs(lfa.mu_loc("jacobi", 0.0, h, 10 / 11, n=1024) - 5 / 11) < 2e-3
+
+
 def test_stencil_support_sizes():
     """9-point (2D) and 19-point (3D) compact stencils; 5/7-point FD2."""
     assert len(L_stencil(2, 1.0)[0]) == 9
