@@ -236,6 +236,13 @@ HMG_API int hmg_stencil_radius(const hmg_hierarchy *hier, int level);
  * coefficient [o][j] multiplies x[j+o]).  Level 0 is materialised from the
  * matrix-free definition.  Returns K or -1. */
 HMG_API int hmg_copy_stencil(const hmg_hierarchy *hier, int level, double *out, int64_t cap_doubles);
+/* Uniform-box compression: the box [lo, hi) of level `level`'s
+ * local node coordinates (x, y, z) in which every stored coefficient equals the
+ * centre node's bit for bit, so the kernels read one shared copy there instead of
+ * the per-node planes.  Returns the number of nodes in the box (0: empty, e.g. a
+ * heterogeneous medium, the coarsest level, or HMG_NO_UNIFORM=1 at build), -1 on
+ * bad arguments.  lo/hi may be NULL. */
+HMG_API int64_t hmg_uniform_box(const hmg_hierarchy *hier, int level, int64_t lo[3], int64_t hi[3]);
 /* Kernel launches issued by this library since load (all entry points). */
 HMG_API int64_t hmg_launch_count(void);
 /* Opt-in per-kernel timing: after hmg_profile_begin(), every solve-path launch

@@ -29,6 +29,8 @@
 #include "k_setup.cuh"
 #include "k_transfer.cuh"
 #include "k_vanka.cuh"
+#include "k_uniform.cuh"
+#include "k_stage3d.cuh"
 
 namespace hmg {
 
@@ -199,6 +201,7 @@ struct SolverBase {
   virtual int radius(int level) const = 0;
   virtual int copy_stencil(int level, double *out, int64_t cap) = 0;
   virtual void level_rows(int level, int64_t *lo, int64_t *hi) const = 0;
+  virtual int64_t uniform_box(int level, int64_t *lo, int64_t *hi) const = 0;
 };
 
 // Slab partition: level-0 rows of the slowest axis split
@@ -248,6 +251,10 @@ template <typename T> struct Solver : SolverBase {
     int64_t lo = 0, hi = 0;     // this rank's global rows on the slab axis
     bool gather_in = false;     // first replicated level: filled by allgather
     Geo view;                   // (gather_in) this rank's owned rows inside the replicated buffer
+    // uniform-box compression (k_uniform.cuh): nodes in ub take their coefficients
+    // from the centre node's copies below instead of the stored planes
+    UBox ub = ubox_empty();
+    std::vector<C> ucoef, ubop;
     std::vector<size_t> goff, glen;   // (gather_in) per-rank byte ranges for the allgather (per element size 1)
   };
   std::vector<Level> lev;
@@ -257,10 +264,16 @@ template <typename T> struct Solver : SolverBase {
   DBuf sigd;              // fine-level sigma in fp64 (restart residual of FGMRES)
   DBuf ainv;              // coarsest inverse, double2 N_L x N_L
   bool rb_closed = false; // fine level uses the closed-form RB patch solve
+  bool stage3d = true;    // 3D fine operator: z-marching staged kernel (HMG_NO_STAGE3D=1 at build: the gather)
   DBuf rb_ia, rb_id;      // its sigma-only factors 1/a_j and 1/(a_c - e^2 sum 1/a_l), stored in T
+  C usig{}, uia{}, uid{};  // level-0 uniform-box values of sig, rb_ia, rb_id
+  D usigd{};
   // FGMRES workspace
   int ws_m = 0;
   DBuf V, Z, partial, dres, io;
+  // address ranges of the solver-owned basis (whole-cycle graphs are captured only for
+  // these: per-call batch states are freed when the call returns)
+  std::pair<const char *, const char *> ownV{nullptr, nullptr}, ownZ{nullptr, nullptr};
   DBuf qd, xd, rd;        // fp64 right-hand side, iterate and restart residual
   int reorth = 0;         // second Gram-Schmidt passes in the last solve
   // CUDA graph of the coarse part of the cycle (levels >= 1 run on fixed
@@ -302,6 +315,7 @@ template <typename T> struct Solver : SolverBase {
     const int dim = opt.dim;
     L = opt.levels;
     G = opt.intergrid == HMG_CUBIC ? 3 : 2;
+    stage3d = std::getenv("HMG_NO_STAGE3D") == nullptr;
     if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
     lev.resize(L);
     int64_t nodes[3] = {opt.cells[0] + 1, opt.cells[1] + 1, dim == 3 ? opt.cells[2] + 1 : 1};
@@ -472,8 +486,113 @@ template <typename T> struct Solver : SolverBase {
     CK(cudaEventCreate(&ev1));
     CK(cudaEventCreateWithFlags(&ev_dots, cudaEventDisableTiming));
     CK(cudaMallocHost((void **)&hpin, 4096 * sizeof(double)));
+    find_uniform(s);
     CK(cudaStreamSynchronize(s));
   }
+
+  // ------------------------------------------------------ uniform-box compression
+  // Per level: the largest box around the centre node in which every stored
+  // coefficient equals the centre node's bit for bit (k_uniform.cuh).  Greedy
+  // growth, one face at a time; every face added is checked whole, so the box
+  // is exact (a valid box, maximal for box-shaped uniform regions such as the
+  // interior of a sponge-bordered homogeneous medium).  HMG_NO_UNIFORM=1 (read
+  // at build) keeps every box empty: the stored path everywhere.
+  template <typename E> void flag_planes(const Geo &g, const DBuf &b, int nplanes, int64_t ref, DBuf &flags,
+                                         cudaStream_t s) {
+    if (!b.p || nplanes <= 0) return;
+    auto nl = node_launch(g);
+    launch(k_uniform_flags<E>, nl.grid, nl.block, 0, s, g, b.template as<E>(), nplanes, ref,
+           flags.template as<unsigned char>());
+  }
+  static UBox grow_box(const std::vector<unsigned char> &f, const int n[3], int dim) {
+    UBox b = ubox_empty();
+    int c[3] = {n[0] / 2, n[1] / 2, dim == 3 ? n[2] / 2 : 0};
+    auto at = [&](int x, int y, int z) { return f[((size_t)z * n[1] + y) * n[0] + x] != 0; };
+    if (!at(c[0], c[1], c[2])) return b;
+    for (int a = 0; a < 3; ++a) { b.lo[a] = c[a]; b.hi[a] = c[a] + 1; }
+    auto face_ok = [&](int a, int v) {   // all nodes of the box's cross-section at coordinate v on axis a
+      int lo[3] = {b.lo[0], b.lo[1], b.lo[2]}, hi[3] = {b.hi[0], b.hi[1], b.hi[2]};
+      lo[a] = v;
+      hi[a] = v + 1;
+      for (int z = lo[2]; z < hi[2]; ++z)
+        for (int y = lo[1]; y < hi[1]; ++y)
+          for (int x = lo[0]; x < hi[0]; ++x)
+            if (!at(x, y, z)) return false;
+      return true;
+    };
+    for (bool grew = true; grew;) {
+      grew = false;
+      for (int a = 0; a < dim; ++a) {
+        if (b.lo[a] > 0 && face_ok(a, b.lo[a] - 1)) { --b.lo[a]; grew = true; }
+        if (b.hi[a] < n[a] && face_ok(a, b.hi[a])) { ++b.hi[a]; grew = true; }
+      }
+    }
+    return b;
+  }
+  void find_uniform(cudaStream_t s) {
+    static_assert(sizeof(C) % 8 == 0, "flag comparison in 8-byte words");
+    const bool off = std::getenv("HMG_NO_UNIFORM") != nullptr;
+    for (int l = 0; l < L; ++l) {
+      Level &Lv = lev[l];
+      Lv.ub = ubox_empty();
+      Lv.ucoef.clear();
+      Lv.ubop.clear();
+      if (off || l == L - 1) continue;   // the coarsest level is a dense inverse
+      const Geo &g = Lv.geo;
+      const int64_t N = g.nodes();
+      const int cx = g.n[0] / 2, cy = g.n[1] / 2, cz = opt.dim == 3 ? g.n[2] / 2 : 0;
+      const int64_t ref = g.idx(cx, cy, cz);
+      DBuf flags;
+      flags.alloc((size_t)N, s);
+      CK(cudaMemsetAsync(flags.p, 1, (size_t)N, s));
+      const int nb = Lv.bop.p ? bstencil_planes() : 0;
+      const int K = l > 0 ? kcount(opt.dim, Lv.r) : 0;
+      if (l == 0) {
+        flag_planes<C>(g, sig, 1, ref, flags, s);
+        flag_planes<D>(g, sigd, 1, ref, flags, s);
+        flag_planes<C>(g, rb_ia, 1, ref, flags, s);
+        flag_planes<C>(g, rb_id, 1, ref, flags, s);
+      } else {
+        flag_planes<C>(g, Lv.coef, K, ref, flags, s);
+      }
+      flag_planes<C>(g, Lv.bop, nb, ref, flags, s);
+      std::vector<unsigned char> hf((size_t)N);
+      CK(cudaMemcpyAsync(hf.data(), flags.p, (size_t)N, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      Lv.ub = grow_box(hf, g.n, opt.dim);
+      if (Lv.ub.nodes() < 64) { Lv.ub = ubox_empty(); continue; }   // not worth a branch
+      auto fetch = [&](const DBuf &b, int nplanes, size_t es, void *dst) {
+        for (int k = 0; k < nplanes; ++k)
+          CK(cudaMemcpyAsync((char *)dst + k * es, (const char *)b.p + ((size_t)k * g.total + ref) * es, es,
+                             cudaMemcpyDeviceToHost, s));
+      };
+      if (l == 0) {
+        fetch(sig, 1, sizeof(C), &usig);
+        fetch(sigd, 1, sizeof(D), &usigd);
+        if (rb_ia.p) fetch(rb_ia, 1, sizeof(C), &uia);
+        if (rb_id.p) fetch(rb_id, 1, sizeof(C), &uid);
+      } else {
+        Lv.ucoef.resize(K);
+        fetch(Lv.coef, K, sizeof(C), Lv.ucoef.data());
+      }
+      if (nb) {
+        Lv.ubop.resize(nb);
+        fetch(Lv.bop, nb, sizeof(C), Lv.ubop.data());
+      }
+      CK(cudaStreamSynchronize(s));
+    }
+  }
+  // kernel-parameter copy of n coefficients (unused entries zero)
+  // kernel-parameter copy in the kernel's ARITHMETIC precision E (exact widening of
+  // the stored values: the same numbers the stored path converts per node)
+  template <int K, typename E = T> static UCoef<K, E> ucopy(const std::vector<C> &v) {
+    UCoef<K, E> u{};
+    for (int k = 0; k < K && k < (int)v.size(); ++k) u.c[k] = mkc<E>((E)v[k].x, (E)v[k].y);
+    return u;
+  }
+  static D widen(const C &c) { return make_double2((double)c.x, (double)c.y); }
+  // coefficient-plane bytes a launch over level l really streams (nodes outside the box)
+  double outside(int l) const { return (double)(lev[l].geo.nodes() - lev[l].ub.nodes()); }
 
   // ---------------------------------------------------------- distribution
   int slab_axis() const { return opt.dim == 3 ? 2 : 1; }
@@ -654,6 +773,32 @@ template <typename T> struct Solver : SolverBase {
     }
   }
 
+  // 3D fine operator y = A x / y = f - A x: the z-marching staged kernel (k_stage3d.cuh)
+  // or the node-parallel gather (bit-identical; HMG_NO_STAGE3D=1)
+  template <typename TT, typename TC, typename TS>
+  void fine3d(const Geo &g, const cplx<TS> *sg, TC a, TC ih2, const cplx<TT> *x, const cplx<TT> *f, cplx<TT> *y,
+              cplx<TC> us, cudaStream_t s) {
+    const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+    const UBox &ub = lev[0].ub;
+    if (!stage3d) {
+      auto nl = node_launch(g);
+      if (c4) launch(k_fine_op<TT, 3, ST_COMPACT4, TC, TS>, nl.grid, nl.block, 0, s, g, sg, a, ih2, x, f, y, ub, us);
+      else launch(k_fine_op<TT, 3, ST_FD2, TC, TS>, nl.grid, nl.block, 0, s, g, sg, a, ih2, x, f, y, ub, us);
+      return;
+    }
+    constexpr int ZC = 32, NS = 4;
+    const int off2 = S3_RY * S3_RX * (int)sizeof(cplx<TT>) + S3_TY * S3_TX * (int)sizeof(cplx<TS>);
+    const int slot = (off2 + (f ? S3_TY * S3_TX * (int)sizeof(cplx<TT>) : 0) + 127) / 128 * 128;
+    const int smem = 128 + NS * slot;
+    const dim3 block(32, 8), grid((g.n[0] + S3_TX - 1) / S3_TX, (g.n[1] + S3_TY - 1) / S3_TY, (g.n[2] + ZC - 1) / ZC);
+    auto go = [&](auto kern) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      launch(kern, grid, block, (size_t)smem, s, g, sg, a, ih2, x, f, y, ub, us);
+    };
+    if (c4) go(k_fine_op3d_z<TT, ST_COMPACT4, TC, TS, ZC, NS>);
+    else go(k_fine_op3d_z<TT, ST_FD2, TC, TS, ZC, NS>);
+  }
+
   // ------------------------------------------------------------ operators
   // Precision model: level-0 vectors are stored in T, vectors
   // of every coarser level in fp64; stencil coefficients and patch factors in
@@ -682,19 +827,19 @@ template <typename T> struct Solver : SolverBase {
     auto nl = node_launch(Lv.geo);
     const double sz = vsize(l), nn = (double)Lv.geo.nodes();
     if (l == 0) {
-      tag(f ? "fine_residual" : "fine_apply", l, (f ? 4 : 3) * sz * nn);
+      tag(f ? "fine_residual" : "fine_apply", l, (f ? 3 : 2) * sz * nn + sz * outside(l));
       const double a = shifted ? alpha : 0.0;
       const double ih2 = 1.0 / (Lv.h * Lv.h);
       const C *sg = sig.template as<C>();
       const C *xx = (const C *)x, *ff = (const C *)f;
       C *yy = (C *)y;
       const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+      const UBox &ub = Lv.ub;
       if (opt.dim == 2) {
-        if (c4) launch(k_fine_op<T, 2, ST_COMPACT4, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy);
-        else launch(k_fine_op<T, 2, ST_FD2, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy);
+        if (c4) launch(k_fine_op<T, 2, ST_COMPACT4, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy, ub, widen(usig));
+        else launch(k_fine_op<T, 2, ST_FD2, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy, ub, widen(usig));
       } else {
-        if (c4) launch(k_fine_op<T, 3, ST_COMPACT4, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy);
-        else launch(k_fine_op<T, 3, ST_FD2, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy);
+        fine3d<T, double, T>(Lv.geo, sg, a, ih2, xx, ff, yy, widen(usig), s);
       }
       return;
     }
@@ -731,11 +876,11 @@ template <typename T> struct Solver : SolverBase {
     const int64_t bs = Lv.geo.total;
     if (opt.dim == 2 && nbat(l) == 1 && std::is_same<T, float>::value && (G % 2) == 0 && Lv.r <= 2 &&
         std::getenv("HMG_NO_PAIR_ST") == nullptr) {   // two nodes per thread, 16-byte coefficient pairs
-      tag(f ? "stored_residual" : "stored_apply", l, kcount(opt.dim, Lv.r) * sizeof(C) * nn + (f ? 3 : 2) * sz * nn);
+      tag(f ? "stored_residual" : "stored_apply", l, kcount(opt.dim, Lv.r) * sizeof(C) * outside(l) + (f ? 3 : 2) * sz * nn);
       const dim3 block(32, 8), grid(((Lv.geo.n[0] + 1) / 2 + 31) / 32, (Lv.geo.n[1] + 7) / 8);
       const float2 *c2 = reinterpret_cast<const float2 *>(cf);
-      if (Lv.r == 1) launch(k_stored_op2d_pair<1>, grid, block, 0, s, Lv.geo, c2, xx, ff, yy);
-      else launch(k_stored_op2d_pair<2>, grid, block, 0, s, Lv.geo, c2, xx, ff, yy);
+      if (Lv.r == 1) launch(k_stored_op2d_pair<1>, grid, block, 0, s, Lv.geo, c2, xx, ff, yy, Lv.ub, ucopy<9, double>(Lv.ucoef));
+      else launch(k_stored_op2d_pair<2>, grid, block, 0, s, Lv.geo, c2, xx, ff, yy, Lv.ub, ucopy<25, double>(Lv.ucoef));
       return;
     }
     over_batch(nbat(l), [&](auto NRc, int q0) {
@@ -743,14 +888,16 @@ template <typename T> struct Solver : SolverBase {
       const D *xq = xx + q0 * bs, *fq = ff ? ff + q0 * bs : nullptr;
       D *yq = yy + q0 * bs;
       tag(f ? "stored_residual" : "stored_apply", l,
-          kcount(opt.dim, Lv.r) * sizeof(C) * nn + (f ? 3 : 2) * sz * nn * NR);
+          kcount(opt.dim, Lv.r) * sizeof(C) * outside(l) + (f ? 3 : 2) * sz * nn * NR);
+      const UBox &ub = Lv.ub;
+      const auto &uv = Lv.ucoef;
       if (opt.dim == 2) {
-        if (Lv.r == 1) launch(k_stored_op<double, T, 2, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
-        else if (Lv.r == 2) launch(k_stored_op<double, T, 2, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
-        else launch(k_stored_op<double, T, 2, 3, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
+        if (Lv.r == 1) launch(k_stored_op<double, T, 2, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<9, double>(uv));
+        else if (Lv.r == 2) launch(k_stored_op<double, T, 2, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<25, double>(uv));
+        else launch(k_stored_op<double, T, 2, 3, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<49, double>(uv));
       } else {
-        if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
-        else launch(k_stored_op<double, T, 3, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs);
+        if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<27, double>(uv));
+        else launch(k_stored_op<double, T, 3, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv));
       }
     });
   }
@@ -834,9 +981,10 @@ template <typename T> struct Solver : SolverBase {
     const int64_t bs = Lv.geo.total;
     over_batch(nbat(l), [&](auto NRc, int q0) {
       constexpr int NR = decltype(NRc)::value;
-      tag(zero ? "vanka_zero" : "vanka", l, ((double)NB * sizeof(C) + (zero ? 2 : 3) * sizeof(TV) * NR) * nn);
+      tag(zero ? "vanka_zero" : "vanka", l, (double)NB * sizeof(C) * outside(l) + (zero ? 2 : 3) * sizeof(TV) * NR * nn);
       launch(k_vanka_stencil<BV, T, DIM, KIND, NR>, nl.grid, nl.block, 0, s, Lv.geo, (const C *)Lv.bop.template as<C>(),
-             (const TV *)r + q0 * bs, (const TV *)u + q0 * bs, (TV *)u + q0 * bs, (BV)damp(l), zero, bs);
+             (const TV *)r + q0 * bs, (const TV *)u + q0 * bs, (TV *)u + q0 * bs, (BV)damp(l), zero, bs, Lv.ub,
+             ucopy<NB, BV>(Lv.ubop));
     });
   }
   template <typename TV> void vanka_kind(int l, const void *r, void *u, int zero, cudaStream_t s) {
@@ -873,7 +1021,9 @@ template <typename T> struct Solver : SolverBase {
       C *uo = (C *)u_out;
       if (!zero) halo(0, u, 3, s);
       halo(0, f, 2, s);
-      tag(zero ? "smooth_rb2d_fine_zero" : "smooth_rb2d_fine", 0, (zero ? 4 : 6) * sizeof(C) * nn);
+      // algorithmic bytes: f, u' (+ u) per node; ia, id (+ sigma) outside the uniform box
+      tag(zero ? "smooth_rb2d_fine_zero" : "smooth_rb2d_fine", 0,
+          (zero ? 2 : 3) * sizeof(C) * nn + (zero ? 2 : 3) * sizeof(C) * outside(0));
       const bool c4 = opt.fine_stencil == HMG_COMPACT4;
       // all arithmetic in fp64 (fp32 patch algebra -- with or
       // without an fp64 residual, in the post-sweep alone -- moved config 0 from
@@ -883,7 +1033,7 @@ template <typename T> struct Solver : SolverBase {
       auto go = [&](auto kern, int na) {
         const int smem = 8 * (PD + 2) * na * 32 * (int)sizeof(C);
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        launch(kern, grid, block, (size_t)smem, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w);
+        launch(kern, grid, block, (size_t)smem, s, Lv.geo, sg, ia, id, alpha, ih2, ff, ui, uo, w, Lv.ub, usig, uia, uid);
       };
       // c64 non-zero: 3 blocks/SM (80 registers) measured 16 % faster than 2 (91 registers)
       constexpr int MB = sizeof(T) == 4 ? 3 : 2;
@@ -896,7 +1046,8 @@ template <typename T> struct Solver : SolverBase {
           const int smem = 4 * (PD + 2) * na * 32 * 16;
           CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
           launch(kern, grid2, block2, (size_t)smem, s, Lv.geo, (const float2 *)sg, (const float2 *)ia,
-                 (const float2 *)id, alpha, ih2, (const float2 *)ff, (const float2 *)ui, (float2 *)uo, w);
+                 (const float2 *)id, alpha, ih2, (const float2 *)ff, (const float2 *)ui, (float2 *)uo, w, Lv.ub,
+                 *(const float2 *)&usig, *(const float2 *)&uia, *(const float2 *)&uid);
         };
         // blocks/SM: zero sweep 4 (126 registers), non-zero 3 (152; 4 spills, measured 2.9x slower)
         // zero sweep: 4 blocks/SM, unrolled x2; non-zero: 3 blocks/SM, unrolled x3 (the
@@ -1128,8 +1279,13 @@ template <typename T> struct Solver : SolverBase {
   void ensure_ws(int m, cudaStream_t s) {
     if (ws_m == m) return;
     const Geo &g = g0();
+    // whole-cycle graphs are keyed on V/Z addresses: drop them with the old buffers
+    for (auto &kv : fgraphs) cudaGraphExecDestroy(kv.second.first);
+    fgraphs.clear();
     V.alloc((size_t)(m + 1) * g.total * sizeof(C), s);
     Z.alloc((size_t)m * g.total * sizeof(C), s);
+    ownV = {(const char *)V.p, (const char *)V.p + V.bytes};
+    ownZ = {(const char *)Z.p, (const char *)Z.p + Z.bytes};
     nblk = (int)std::min<int64_t>(148 * 8, (g.slab_len + KRY_THREADS - 1) / KRY_THREADS);
     partial.alloc((size_t)KRY_MAXV * KRY_MAXBLK * sizeof(double2), s);
     dres.alloc(256 * sizeof(double2), s);
@@ -1193,22 +1349,22 @@ template <typename T> struct Solver : SolverBase {
     auto nl = node_launch(Lv.geo);
     const double ih2 = 1.0 / (Lv.h * Lv.h);
     const double2 *sg = sigd.template as<double2>();
-    tag("fine_apply", 0, (2.0 * sizeof(C) + sizeof(double2)) * Lv.geo.nodes());
+    tag("fine_apply", 0, 2.0 * sizeof(C) * Lv.geo.nodes() + sizeof(double2) * outside(0));
     const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+    const UBox &ub = Lv.ub;
     if (pair_ok()) {
       const dim3 block(32, 8), grid(((Lv.geo.n[0] + 1) / 2 + 31) / 32, (Lv.geo.n[1] + 7) / 8);
       const float2 *zz = reinterpret_cast<const float2 *>(z);
       float2 *ww = reinterpret_cast<float2 *>(w);
-      if (c4) launch(k_fine_op2d_pair<ST_COMPACT4, double, double>, grid, block, 0, s, Lv.geo, sg, 0.0, ih2, zz, (const float2 *)nullptr, ww);
-      else launch(k_fine_op2d_pair<ST_FD2, double, double>, grid, block, 0, s, Lv.geo, sg, 0.0, ih2, zz, (const float2 *)nullptr, ww);
+      if (c4) launch(k_fine_op2d_pair<ST_COMPACT4, double, double>, grid, block, 0, s, Lv.geo, sg, 0.0, ih2, zz, (const float2 *)nullptr, ww, ub, usigd);
+      else launch(k_fine_op2d_pair<ST_FD2, double, double>, grid, block, 0, s, Lv.geo, sg, 0.0, ih2, zz, (const float2 *)nullptr, ww, ub, usigd);
       return;
     }
     if (opt.dim == 2) {
-      if (c4) launch(k_fine_op<T, 2, ST_COMPACT4, double, double>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, z, (const C *)nullptr, w);
-      else launch(k_fine_op<T, 2, ST_FD2, double, double>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, z, (const C *)nullptr, w);
+      if (c4) launch(k_fine_op<T, 2, ST_COMPACT4, double, double>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, z, (const C *)nullptr, w, ub, usigd);
+      else launch(k_fine_op<T, 2, ST_FD2, double, double>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, z, (const C *)nullptr, w, ub, usigd);
     } else {
-      if (c4) launch(k_fine_op<T, 3, ST_COMPACT4, double, double>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, z, (const C *)nullptr, w);
-      else launch(k_fine_op<T, 3, ST_FD2, double, double>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, z, (const C *)nullptr, w);
+      fine3d<T, double, double>(Lv.geo, sg, 0.0, ih2, z, (const C *)nullptr, w, usigd, s);
     }
   }
 
@@ -1221,14 +1377,14 @@ template <typename T> struct Solver : SolverBase {
     const double2 *sg = sigd.template as<double2>();
     const double2 *x = xd.template as<double2>(), *f = qd.template as<double2>();
     double2 *y = rd.template as<double2>();
-    tag("fine_residual_fp64", 0, 64.0 * Lv.geo.nodes());
+    tag("fine_residual_fp64", 0, 48.0 * Lv.geo.nodes() + 16.0 * outside(0));
     const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+    const UBox &ub = Lv.ub;
     if (opt.dim == 2) {
-      if (c4) launch(k_fine_op<double, 2, ST_COMPACT4>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y);
-      else launch(k_fine_op<double, 2, ST_FD2>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y);
+      if (c4) launch(k_fine_op<double, 2, ST_COMPACT4>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y, ub, usigd);
+      else launch(k_fine_op<double, 2, ST_FD2>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y, ub, usigd);
     } else {
-      if (c4) launch(k_fine_op<double, 3, ST_COMPACT4>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y);
-      else launch(k_fine_op<double, 3, ST_FD2>, nl.grid, nl.block, 0, s, Lv.geo, sg, 0.0, ih2, x, f, y);
+      fine3d<double, double, double>(Lv.geo, sg, 0.0, ih2, x, f, y, usigd, s);
     }
   }
 
@@ -1253,6 +1409,16 @@ template <typename T> struct Solver : SolverBase {
     std::swap(xd, r.xd);
     std::swap(rd, r.rd);
   }
+  // binds a state for one scope and unbinds it on exit, also when the scope
+  // throws (breakdown, CUDA error): the state's buffers never stay swapped in
+  struct Bound {
+    Solver *sv;
+    RhsState &r;
+    Bound(Solver *sv_, RhsState &r_) : sv(sv_), r(r_) { sv->bind(r); }
+    ~Bound() { sv->bind(r); }
+    Bound(const Bound &) = delete;
+    Bound &operator=(const Bound &) = delete;
+  };
   // the state's own buffers (the first state of a solve borrows the solver's)
   void alloc_state(RhsState &r, int m, cudaStream_t s) {
     const Geo &g = g0();
@@ -1269,8 +1435,11 @@ template <typename T> struct Solver : SolverBase {
   void cycle_batch(const std::vector<const C *> &f, const std::vector<C *> &u, cudaStream_t s) {
     const int na = (int)f.size();
     if (na == 1 || L < 2) {
+      auto owned = [](const void *p, const std::pair<const char *, const char *> &r) {
+        return (const char *)p >= r.first && (const char *)p < r.second;
+      };
       for (int k = 0; k < na; ++k) {
-        if (full_graph_ok()) full_cycle_graph(f[k], u[k], s);
+        if (full_graph_ok() && owned(f[k], ownV) && owned(u[k], ownZ)) full_cycle_graph(f[k], u[k], s);
         else cycle(0, f[k], u[k], 1, s);
       }
       return;
@@ -1464,10 +1633,11 @@ template <typename T> struct Solver : SolverBase {
       r.y.assign(m, cd(0, 0));
       r.nbeta.assign(m + 1, 1.0);
       r.hist.assign(1, 1.0);
-      bind(r);
-      CK(cudaMemsetAsync(xd.p, 0, g0().total * sizeof(double2), s));
-      r.qn = norm<double>(qd.template as<double2>(), s);
-      bind(r);
+      {
+        Bound b(this, r);
+        CK(cudaMemsetAsync(xd.p, 0, g0().total * sizeof(double2), s));
+        r.qn = norm<double>(qd.template as<double2>(), s);
+      }
       if (r.qn == 0.0) { r.active = false; r.converged = true; r.true_rel = 0.0; r.est = 0.0; }
       if (maxiter == 0) r.active = false;
     }
@@ -1479,9 +1649,8 @@ template <typename T> struct Solver : SolverBase {
       for (auto &r : st) {
         if (!r.active) continue;
         if (r.start) {
-          bind(r);
+          Bound b(this, r);
           fgmres_start(r, tol, s);
-          bind(r);
         }
         if (r.active) act.push_back(&r);
       }
@@ -1495,9 +1664,8 @@ template <typename T> struct Solver : SolverBase {
       const bool single = act.size() == 1 && std::getenv("HMG_NO_PIPELINE") == nullptr;
       if (!(single && act[0]->pre)) cycle_batch(fv, uv, s);   // (already enqueued when pipelined)
       for (RhsState *r : act) {
-        bind(*r);
+        Bound b(this, *r);
         fgmres_step(*r, tol, maxiter, s, single);
-        bind(*r);
       }
     }
   }
@@ -1537,7 +1705,8 @@ template <typename T> struct Solver : SolverBase {
     const int64_t N = g.nodes();
     auto nl = node_launch(g);
     std::vector<RhsState> st(nr);
-    bind(st[0]);                                      // the first state borrows the solver's buffers
+    // the first state borrows the solver's buffers until this call returns or throws
+    Bound borrow(this, st[0]);
     for (int k = 1; k < nr; ++k) alloc_state(st[k], m, s);
     for (int k = 0; k < nr; ++k) {
       const C *qsrc = (const C *)q + (size_t)k * N;
@@ -1550,12 +1719,7 @@ template <typename T> struct Solver : SolverBase {
     }
     CK(cudaEventRecord(ev0, s));
     hmg_status st_out = HMG_OK;
-    try {
-      fgmres(st, m, tol, maxiter, s);
-    } catch (...) {
-      bind(st[0]);                                    // give the borrowed buffers back
-      throw;
-    }
+    fgmres(st, m, tol, maxiter, s);
     CK(cudaEventRecord(ev1, s));
     for (int k = 0; k < nr; ++k) {
       C *xdst = host ? io.template as<C>() : (C *)x + (size_t)k * N;
@@ -1566,7 +1730,6 @@ template <typename T> struct Solver : SolverBase {
       if (!st[k].converged) st_out = HMG_ENOTCONVERGED;
     }
     CK(cudaStreamSynchronize(s));
-    bind(st[0]);                                      // give the borrowed buffers back
     if (reps) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, ev0, ev1));
@@ -1583,6 +1746,14 @@ template <typename T> struct Solver : SolverBase {
     return g.nodes();
   }
   int radius(int l) const override { return (l < 0 || l >= L) ? -1 : lev[l].r; }
+  int64_t uniform_box(int l, int64_t *lo, int64_t *hi) const override {
+    if (l < 0 || l >= L) return -1;
+    for (int a = 0; a < 3; ++a) {
+      if (lo) lo[a] = lev[l].ub.lo[a];
+      if (hi) hi[a] = lev[l].ub.hi[a];
+    }
+    return lev[l].ub.nodes();
+  }
   void level_rows(int l, int64_t *lo, int64_t *hi) const override {
     if (l < 0 || l >= L) { *lo = *hi = -1; return; }
     *lo = lev[l].lo;
@@ -1857,6 +2028,10 @@ int hmg_copy_stencil(const hmg_hierarchy *h, int level, double *out, int64_t cap
     t_err = e.what();
     return -1;
   }
+}
+
+int64_t hmg_uniform_box(const hmg_hierarchy *h, int level, int64_t lo[3], int64_t hi[3]) {
+  return h ? h->impl->uniform_box(level, lo, hi) : -1;
 }
 
 int64_t hmg_launch_count(void) { return hmg::g_launches.load(); }

@@ -14,6 +14,7 @@
 // layer of the padded box (truncation = homogeneous Dirichlet).
 #pragma once
 #include "common.cuh"
+#include "k_uniform.cuh"
 
 namespace hmg {
 
@@ -44,10 +45,11 @@ template <> struct FineW<3, ST_FD2> {
 // TS = storage precision of sigma.
 // (A x)_i or (f - A x)_i at padded index i, rounded to T (shared by every kernel
 // that forms the fine operator, so their results agree bit for bit)
+// uni: the node lies in the level's uniform box, sigma = us (k_uniform.cuh)
 template <typename T, int DIM, int KIND, typename TC, typename TS>
 __device__ __forceinline__ cplx<T> fine_op_node(const Geo &g, const cplx<TS> *__restrict__ sig, TC alpha, TC ih2,
                                                 const cplx<T> *__restrict__ x, const cplx<T> *__restrict__ f,
-                                                int64_t i) {
+                                                int64_t i, bool uni = false, cplx<TC> us = cplx<TC>{}) {
   using W = FineW<DIM, KIND>;
   using CC = cplx<TC>;
   const int64_t px = g.px;
@@ -74,7 +76,7 @@ __device__ __forceinline__ cplx<T> fine_op_node(const Geo &g, const cplx<TS> *__
   // M x
   CC Mx = cscale<TC>(xc, (TC)W::Mc);
   if (W::Mf != 0.0) Mx = cfmar<TC>(Mx, (TC)W::Mf, sf);
-  CC s = ccast<TC, TS>(sig[i]);
+  CC s = uni ? us : ccast<TC, TS>(sig[i]);   // (uniform value kept in TC: no conversion)
   s.y = fma(-alpha, s.x, s.y);
   const CC Ax = csub<TC>(Lx, cmul<TC>(s, Mx));
   return ccast<T, TC>(f ? csub<TC>(ccast<TC, T>(f[i]), Ax) : Ax);
@@ -83,10 +85,11 @@ __device__ __forceinline__ cplx<T> fine_op_node(const Geo &g, const cplx<TS> *__
 template <typename T, int DIM, int KIND, typename TC = T, typename TS = T>
 __global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<TS> *__restrict__ sig, TC alpha, TC ih2,
                                                  const cplx<T> *__restrict__ x,
-                                                 const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y) {
+                                                 const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y,
+                                                 UBox ub, cplx<TC> us) {
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t i = g.idx(ix, iy, iz);
-  y[i] = fine_op_node<T, DIM, KIND, TC, TS>(g, sig, alpha, ih2, x, f, i);
+  y[i] = fine_op_node<T, DIM, KIND, TC, TS>(g, sig, alpha, ih2, x, f, i, ub.in(ix, iy, iz), us);
 }
 
 // 2D c64 variant of k_fine_op: one thread per PAIR of x-adjacent nodes
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<TS> *__restri
 template <int KIND, typename TC, typename TSG>
 __global__ void __launch_bounds__(256) k_fine_op2d_pair(Geo g, const cplx<TSG> *__restrict__ sig, TC alpha, TC ih2,
                                                         const float2 *__restrict__ x, const float2 *__restrict__ f,
-                                                        float2 *__restrict__ y) {
+                                                        float2 *__restrict__ y, UBox ub, cplx<TC> us) {
   using W = FineW<2, KIND>;
   using CC = cplx<TC>;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -135,7 +138,8 @@ __global__ void __launch_bounds__(256) k_fine_op2d_pair(Geo g, const cplx<TSG> *
     Ma = cfmar<TC>(Ma, (TC)W::Mf, sfa);
     Mb = cfmar<TC>(Mb, (TC)W::Mf, sfb);
   }
-  CC sga = ccast<TC, TSG>(sig[i]), sgb = ccast<TC, TSG>(sig[i + 1]);
+  const bool ua = ub.in(x0, iy, 0), ubb = ub.in(x0 + 1, iy, 0);
+  CC sga = ua ? us : ccast<TC, TSG>(sig[i]), sgb = ubb ? us : ccast<TC, TSG>(sig[i + 1]);
   sga.y = fma(-alpha, sga.x, sga.y);
   sgb.y = fma(-alpha, sgb.x, sgb.y);
   CC oa = csub<TC>(La, cmul<TC>(sga, Ma)), ob = csub<TC>(Lb, cmul<TC>(sgb, Mb));
@@ -153,32 +157,41 @@ __global__ void __launch_bounds__(256) k_fine_op2d_pair(Geo g, const cplx<TSG> *
 // Stored stencil of radius R: coef[k][j], k = (ox+R) + (2R+1)((oy+R) + (2R+1)(oz+R)),
 // multiplies x[j + o].  Coefficients towards out-of-domain nodes are zero.
 // TV = vector storage/arithmetic (fp64 on Galerkin levels), TK = coefficient storage.
+template <int DIM, int R> constexpr int kplanes() { return DIM == 3 ? (2 * R + 1) * (2 * R + 1) * (2 * R + 1) : (2 * R + 1) * (2 * R + 1); }
+
 template <typename TV, typename TK, int DIM, int R, int NR = 1>
 __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__restrict__ coef,
                                                    const cplx<TV> *__restrict__ x,
                                                    const cplx<TV> *__restrict__ f, cplx<TV> *__restrict__ y,
-                                                   int64_t bs = 0) {
+                                                   int64_t bs, UBox ub, UCoef<kplanes<DIM, R>(), TV> uc) {
   // NR right-hand sides at a stride of bs elements: each coefficient is read once
   // and applied to all of them (multi-RHS batches; same per-RHS arithmetic order)
   using T = TV;
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t i = g.idx(ix, iy, iz);
+  const bool uni = ub.in(ix, iy, iz);   // coefficients from the uniform-box copy (k_uniform.cuh)
   constexpr int ZR = DIM == 3 ? R : 0;
   cplx<T> acc[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r] = mkc<T>(0, 0);
-  int k = 0;
+  // two copies of the unrolled loop behind a branch (not a per-coefficient select:
+  // predicated-off loads and conversions would still take issue slots)
+  auto run = [&](auto coef_k) {
+    int k = 0;
 #pragma unroll
-  for (int oz = -ZR; oz <= ZR; ++oz)
+    for (int oz = -ZR; oz <= ZR; ++oz)
 #pragma unroll
-    for (int oy = -R; oy <= R; ++oy)
+      for (int oy = -R; oy <= R; ++oy)
 #pragma unroll
-      for (int ox = -R; ox <= R; ++ox, ++k) {
-        const cplx<T> c = ccast<T, TK>(coef[(int64_t)k * g.total + i]);
-        const int64_t j = i + g.delta(ox, oy, oz);
+        for (int ox = -R; ox <= R; ++ox, ++k) {
+          const cplx<T> c = coef_k(k);
+          const int64_t j = i + g.delta(ox, oy, oz);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) acc[r] = cfma<T>(acc[r], c, x[r * bs + j]);
-      }
+          for (int r = 0; r < NR; ++r) acc[r] = cfma<T>(acc[r], c, x[r * bs + j]);
+        }
+  };
+  if (uni) run([&](int k) { return uc.c[k]; });
+  else run([&](int k) { return ccast<T, TK>(coef[(int64_t)k * g.total + i]); });
 #pragma unroll
   for (int r = 0; r < NR; ++r) y[r * bs + i] = f ? csub<T>(f[r * bs + i], acc[r]) : acc[r];
 }
@@ -190,7 +203,8 @@ __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__rest
 template <int R>
 __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *__restrict__ coef,
                                                           const double2 *__restrict__ x,
-                                                          const double2 *__restrict__ f, double2 *__restrict__ y) {
+                                                          const double2 *__restrict__ f, double2 *__restrict__ y,
+                                                          UBox ub, UCoef<(2 * R + 1) * (2 * R + 1), double> uc) {
   using T = double;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int iy = blockIdx.y * blockDim.y + threadIdx.y;
@@ -198,20 +212,35 @@ __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *_
   if (ix >= g.n[0] || iy >= g.n[1]) return;
   const int64_t i = g.idx(ix, iy, 0);
   const bool two = ix + 1 < g.n[0];
+  const bool uni = ub.in(ix, iy, 0) && (!two || ub.in(ix + 1, iy, 0));   // both nodes in the uniform box
   double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
-  int k = 0;
+  // uniform box: fp64 coefficient copies from the parameter bank, no loads, no
+  // conversions -- a separate copy of the unrolled loop behind one branch
+  auto run = [&](auto coef_k) {
+    int k = 0;
 #pragma unroll
-  for (int oy = -R; oy <= R; ++oy) {
-    const double2 *row = x + i + (int64_t)oy * g.px;
-    double2 xw[2 * R + 2];
+    for (int oy = -R; oy <= R; ++oy) {
+      const double2 *row = x + i + (int64_t)oy * g.px;
+      double2 xw[2 * R + 2];
 #pragma unroll
-    for (int c = 0; c < 2 * R + 2; ++c) xw[c] = row[c - R];
+      for (int c = 0; c < 2 * R + 2; ++c) xw[c] = row[c - R];
 #pragma unroll
-    for (int ox = -R; ox <= R; ++ox, ++k) {
-      const float4 c2 = *reinterpret_cast<const float4 *>(coef + (int64_t)k * g.total + i);
-      a0 = cfma<T>(a0, mkc<T>(c2.x, c2.y), xw[ox + R]);
-      a1 = cfma<T>(a1, mkc<T>(c2.z, c2.w), xw[ox + R + 1]);
+      for (int ox = -R; ox <= R; ++ox, ++k) {
+        double2 k0, k1;
+        coef_k(k, k0, k1);
+        a0 = cfma<T>(a0, k0, xw[ox + R]);
+        a1 = cfma<T>(a1, k1, xw[ox + R + 1]);
+      }
     }
+  };
+  if (uni) {
+    run([&](int k, double2 &k0, double2 &k1) { k0 = k1 = uc.c[k]; });
+  } else {
+    run([&](int k, double2 &k0, double2 &k1) {
+      const float4 c2 = *reinterpret_cast<const float4 *>(coef + (int64_t)k * g.total + i);
+      k0 = mkc<T>(c2.x, c2.y);
+      k1 = mkc<T>(c2.z, c2.w);
+    });
   }
   y[i] = f ? csub<T>(f[i], a0) : a0;
   if (two) y[i + 1] = f ? csub<T>(f[i + 1], a1) : a1;

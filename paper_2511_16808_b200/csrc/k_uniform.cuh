@@ -1,0 +1,65 @@
+// k_uniform.cuh -- uniform-box coefficient compression.
+//
+// Where the medium is uniform (kappa constant, gamma = 0: the interior of the
+// homogeneous configurations 0, 1, 3 and of the paper's Tables 5.2 / 5.4
+// experiments), every per-node coefficient of a level -- sigma and
+// the RB factors on the fine level, the Galerkin stencil A_l = R A P
+// and the assembled additive Vanka operator B_l (Eq. 3.8) on the
+// others -- is the SAME value at every node of an interior box: it is computed
+// by the same fp64 arithmetic from the same neighbourhood values.  Setup finds
+// that box per level by comparing every node's coefficients bit for bit with
+// those of the level's centre node (k_uniform_flags + the host box search);
+// the kernels then take a node's coefficients from a kernel-parameter copy of
+// the centre node's values (constant bank, broadcast) when the node lies in
+// the box and load the stored planes only outside it (sponge, boundary rows,
+// heterogeneous media).  Same values, same arithmetic order: the output is bit
+// identical to the stored path (tests/test_gpu_uniform.py); heterogeneous media
+// get an empty box and run the stored path unchanged.
+#pragma once
+#include "common.cuh"
+
+namespace hmg {
+
+// half-open box of LOCAL interior node coordinates (empty: lo = hi = 0)
+struct UBox {
+  int lo[3], hi[3];
+  __host__ __device__ __forceinline__ bool in(int x, int y, int z) const {
+    return x >= lo[0] && x < hi[0] && y >= lo[1] && y < hi[1] && z >= lo[2] && z < hi[2];
+  }
+  __host__ __device__ __forceinline__ bool empty() const {
+    return lo[0] >= hi[0] || lo[1] >= hi[1] || lo[2] >= hi[2];
+  }
+  __host__ __device__ __forceinline__ int64_t nodes() const {
+    return empty() ? 0 : (int64_t)(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
+  }
+};
+inline UBox ubox_empty() {
+  UBox b;
+  for (int a = 0; a < 3; ++a) b.lo[a] = b.hi[a] = 0;
+  return b;
+}
+
+// the box's copy of K complex coefficients (kernel parameter; indices are
+// compile-time constants after unrolling, so reads are constant-bank operands)
+template <int K, typename TK> struct UCoef {
+  cplx<TK> c[K];
+};
+
+// flag[j] &= (all nplanes values of node j equal those of node ref), bitwise
+template <typename E>
+__global__ void k_uniform_flags(Geo g, const E *__restrict__ planes, int nplanes, int64_t ref,
+                                unsigned char *__restrict__ flag) {
+  HMG_NODE_IDX(g, ix, iy, iz);
+  const int64_t j = g.idx(ix, iy, iz);
+  const int64_t f = ((int64_t)iz * g.n[1] + iy) * g.n[0] + ix;
+  if (!flag[f]) return;
+  const unsigned long long *p = reinterpret_cast<const unsigned long long *>(planes);
+  constexpr int W = sizeof(E) / 8;
+  bool same = true;
+  for (int k = 0; k < nplanes && same; ++k)
+    for (int w = 0; w < W; ++w)
+      same = same && p[((int64_t)k * g.total + j) * W + w] == p[((int64_t)k * g.total + ref) * W + w];
+  if (!same) flag[f] = 0;
+}
+
+}  // namespace hmg

@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "k_operator.cuh"
+#include "k_uniform.cuh"
 
 namespace hmg {
 
@@ -138,20 +139,27 @@ __device__ __forceinline__ void static_for(F &&f) {
 template <typename T, typename TK, int DIM, int KIND, int NR = 1>
 __global__ void __launch_bounds__(256) k_vanka_stencil(Geo g, const cplx<TK> *__restrict__ B,
                                                        const cplx<T> *__restrict__ r, const cplx<T> *u,
-                                                       cplx<T> *u_out, T w, int zero, int64_t bs = 0) {
+                                                       cplx<T> *u_out, T w, int zero, int64_t bs, UBox ub,
+                                                       UCoef<BStencil<DIM, KIND>::NB, T> uc) {
   HMG_NODE_IDX(g, ix, iy, iz);
   using S = BStencil<DIM, KIND>;
   const int64_t j = g.idx(ix, iy, iz);
+  const bool uni = ub.in(ix, iy, iz);   // B from the uniform-box copy (k_uniform.cuh)
   cplx<T> acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = mkc<T>(0, 0);
-  static_for<0, S::NB>([&](auto P) {
-    constexpr int p = decltype(P)::value;
-    const cplx<T> b = ccast<T, TK>(B[(int64_t)p * g.total + j]);
-    const int64_t o = j + g.delta(S::template dx<p>, S::template dy<p>, S::template dz<p>);
+  // uniform box: B from the parameter copy (in T); a separate loop copy behind one branch
+  auto run = [&](auto bcoef) {
+    static_for<0, S::NB>([&](auto P) {
+      constexpr int p = decltype(P)::value;
+      const cplx<T> b = bcoef(p);
+      const int64_t o = j + g.delta(S::template dx<p>, S::template dy<p>, S::template dz<p>);
 #pragma unroll
-    for (int q = 0; q < NR; ++q) acc[q] = cfma<T>(acc[q], b, r[q * bs + o]);
-  });
+      for (int q = 0; q < NR; ++q) acc[q] = cfma<T>(acc[q], b, r[q * bs + o]);
+    });
+  };
+  if (uni) run([&](int p) { return uc.c[p]; });
+  else run([&](int p) { return ccast<T, TK>(B[(int64_t)p * g.total + j]); });
   // explicit fma / mul: the same rounding in every batch-width instantiation
   // (left to the compiler, u + w acc is contracted in some and not in others)
 #pragma unroll
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
                                                     const cplx<TS> *__restrict__ ia_, const cplx<TS> *__restrict__ id_,
                                                     double alpha_d, double ih2_d, const cplx<TS> *__restrict__ f,
                                                     const cplx<TS> *__restrict__ u, cplx<TS> *__restrict__ u_out,
-                                                    double w_d) {
+                                                    double w_d, UBox ub, cplx<TS> usg, cplx<TS> uia, cplx<TS> uid) {
   using W = FineW<2, KIND>;
   using D = TC;
   const D alpha = (D)alpha_d, ih2 = (D)ih2_d, w = (D)w_d;
@@ -256,8 +264,13 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
   const CD z = mkc<D>(0, 0);
   // x validity is fixed per lane; rows are checked against the global slab range
   const bool xin = x + g.o[0] >= 0 && x + g.o[0] < g.N[0];
-  const int ylo = -g.o[1], yhi = g.N[1] - g.o[1];
+  // rows are also clamped to y1 + 2, the last row the outputs need (u at yo + 3 for
+  // output yo <= y1 - 1): rows past it may lie beyond this rank's ghosted box
+  const int ylo = -g.o[1], yhi = min(g.N[1] - g.o[1], y1 + 3), ydom = g.N[1] - g.o[1];
   auto in = [&](int y) { return xin && y >= ylo && y < yhi; };
+  // uniform box (k_uniform.cuh): sigma, ia, id of row y come from the box's copies
+  const bool xuni = x >= ub.lo[0] && x < ub.hi[0];
+  auto urow = [&](int y) { return xuni && y >= ub.lo[1] && y < ub.hi[1]; };
   // rolling window (u and ia stay in their storage type: converting on use is
   // exact and keeps the register count down)
   using CS = cplx<TS>;
@@ -302,11 +315,11 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
     const int b_ = y0 - 2 + it_, slot = it_ % NST;
     const int64_t o = ob0 + (int64_t)it_ * px;
     cp(f, b_, o, slot, 0);
-    cp(ia_, b_, o, slot, 1);
-    cp(id_, b_ - 1, o - px, slot, 2);
+    if (!urow(b_)) cp(ia_, b_, o, slot, 1);
+    if (!urow(b_ - 1)) cp(id_, b_ - 1, o - px, slot, 2);
     if (!ZERO) {
       cp(u, b_ + 1, o + px, slot, 3);
-      cp(sig, b_, o, slot, 4);
+      if (!urow(b_)) cp(sig, b_, o, slot, 4);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -325,9 +338,10 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
       ub1 = um1;
       um1 = u0; u0 = up1; up1 = sl[3 * 32];
     }
-    const CS pf_cur = sl[0], ps_cur = ZERO ? zs : sl[4 * 32];
-    const CD fb = ccast<D, TS>(pf_cur), idb = ccast<D, TS>(sl[2 * 32]);
-    const CS ab = sl[32];
+    const bool ub_ = urow(b);
+    const CS pf_cur = sl[0], ps_cur = ZERO ? zs : (ub_ ? usg : sl[4 * 32]);
+    const CD fb = ccast<D, TS>(pf_cur), idb = ccast<D, TS>(urow(b - 1) ? uid : sl[2 * 32]);
+    const CS ab = ub_ ? uia : sl[32];
     // ---- r(b) in TR, t(b).  L u in difference form, sum w (u_nb - u_c): exact
     // algebra because Lc + 4 Lf + 4 Le = 0 (zero ghosts included), and it keeps
     // the cancellation of the compact stencil out of a low-precision sum.
@@ -379,7 +393,7 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
         // y_c vanishes outside the domain, so the sums need no masking, only the count
         const CD syl = cadd<D>(g3, g1);
         const bool xm = x - 1 + g.o[0] >= 0, xp = x + 1 + g.o[0] < g.N[0];
-        const bool ym = yo - 1 >= ylo, yp = yo + 1 < yhi;
+        const bool ym = yo - 1 >= ylo, yp = yo + 1 < ydom;
         const int k = (int)(xm && ym) + (int)(xp && ym) + (int)(xm && yp) + (int)(xp && yp);
         const D kd = (D)kRbCount[k];
         const CD lv = cmul<D>(mkc<D>(kd * r2.x - e * syl.x, kd * r2.y - e * syl.y), ccast<D, TS>(a2));
@@ -403,7 +417,7 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
                                                            const float2 *__restrict__ id_, double alpha_d,
                                                            double ih2_d, const float2 *__restrict__ f,
                                                            const float2 *__restrict__ u, float2 *__restrict__ u_out,
-                                                           double w_d) {
+                                                           double w_d, UBox ub, float2 usg, float2 uia, float2 uid) {
   using W = FineW<2, KIND>;
   using D = double;
   using CD = double2;
@@ -427,8 +441,12 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
   const D e = W::Le * ih2;
   const CD z = mkc<D>(0, 0);
   const CS zs = mkc<float>(0, 0);
-  const int ylo = -g.o[1], yhi = g.N[1] - g.o[1];
+  // rows clamped to y1 + 2 as in k_rb2d_march (beyond it: possibly past this rank's box)
+  const int ylo = -g.o[1], yhi = min(g.N[1] - g.o[1], y1 + 3), ydom = g.N[1] - g.o[1];
   auto yok = [&](int y) { return y >= ylo && y < yhi; };
+  // uniform box (k_uniform.cuh): both columns inside -> sigma, ia, id of row y from the box's copies
+  const bool xuni = x0 >= ub.lo[0] && x0 + 1 < ub.hi[0];
+  auto urow = [&](int y) { return xuni && y >= ub.lo[1] && y < ub.hi[1]; };
   CS um1[2] = {zs, zs}, u0[2] = {zs, zs}, up1[2] = {zs, zs}, ub1[2] = {zs, zs};
   CD r2[2] = {z, z}, r1[2] = {z, z}, r0[2] = {z, z};
   CD h2[2] = {z, z}, h1[2] = {z, z}, h0[2] = {z, z};
@@ -463,11 +481,11 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
     const int b_ = y0 - 2 + it_, slot = it_ % NST;
     const int64_t o = ob0 + (int64_t)it_ * px;
     cp(f, b_, o, slot, 0);
-    cp(ia_, b_, o, slot, 1);
-    cp(id_, b_ - 1, o - px, slot, 2);
+    if (!urow(b_)) cp(ia_, b_, o, slot, 1);
+    if (!urow(b_ - 1)) cp(id_, b_ - 1, o - px, slot, 2);
     if (!ZERO) {
       cp(u, b_ + 1, o + px, slot, 3);
-      cp(sig, b_, o, slot, 4);
+      if (!urow(b_)) cp(sig, b_, o, slot, 4);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -486,14 +504,15 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
     const float4 *sl = ring + (it % NST) * NA * 32 + lane;
     auto split = [](float4 v, CS &p0, CS &p1) { p0 = mkc<float>(v.x, v.y); p1 = mkc<float>(v.z, v.w); };
     CS fv[2], av[2], dv[2], sv[2] = {zs, zs};
+    const bool ub_ = urow(b), ubm = urow(b - 1);
     split(sl[0], fv[0], fv[1]);
-    split(sl[32], av[0], av[1]);
-    split(sl[64], dv[0], dv[1]);
+    split(ub_ ? make_float4(uia.x, uia.y, uia.x, uia.y) : sl[32], av[0], av[1]);
+    split(ubm ? make_float4(uid.x, uid.y, uid.x, uid.y) : sl[64], dv[0], dv[1]);
     if (!ZERO) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) { ub1[q] = um1[q]; um1[q] = u0[q]; u0[q] = up1[q]; }
       split(sl[96], up1[0], up1[1]);
-      split(sl[128], sv[0], sv[1]);
+      split(ub_ ? make_float4(usg.x, usg.y, usg.x, usg.y) : sl[128], sv[0], sv[1]);
     }
     CD rb[2];
 #pragma unroll
@@ -556,7 +575,7 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
         const CD syl = cadd<D>(g3[q], g1[q]);
         const int xq = x0 + q + g.o[0];
         const bool xm = xq - 1 >= 0, xp = xq + 1 < g.N[0];
-        const bool ym = yo - 1 >= ylo, yp = yo + 1 < yhi;
+        const bool ym = yo - 1 >= ylo, yp = yo + 1 < ydom;
         const int k = (int)(xm && ym) + (int)(xp && ym) + (int)(xm && yp) + (int)(xp && yp);
         const D kd = (D)kRbCount[k];
         const CD lv = cmul<D>(mkc<D>(kd * r2[q].x - e * syl.x, kd * r2[q].y - e * syl.y), ccast<D, float>(a2[q]));

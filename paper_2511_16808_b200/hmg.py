@@ -74,6 +74,7 @@ _sigs = {
     "hmg_level_nodes": ([_vp, _i, ctypes.POINTER(_i64)], _i64),
     "hmg_stencil_radius": ([_vp, _i], _i),
     "hmg_copy_stencil": ([_vp, _i, ctypes.POINTER(_d), _i64], _i),
+    "hmg_uniform_box": ([_vp, _i, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i64),
     "hmg_launch_count": ([], _i64),
     "hmg_profile_begin": ([], None),
     "hmg_profile_report": ([], ctypes.c_char_p),
@@ -298,6 +299,14 @@ class Hierarchy:
         if _lib.hmg_level_rows(self._h, level, ctypes.byref(lo), ctypes.byref(hi)) != 0:
             raise HmgError(EINVAL, "level out of range")
         return lo.value, hi.value
+
+    def uniform_box(self, level):
+        """(nodes, lo, hi) of the level's uniform-coefficient box."""
+        lo, hi = (ctypes.c_int64 * 3)(), (ctypes.c_int64 * 3)()
+        n = _lib.hmg_uniform_box(self._h, level, lo, hi)
+        if n < 0:
+            raise HmgError(EINVAL, "level out of range")
+        return int(n), tuple(lo[a] for a in range(self.opts.dim)), tuple(hi[a] for a in range(self.opts.dim))
 
     def stencil_radius(self, level):
         return int(_lib.hmg_stencil_radius(self._h, level))
