@@ -18,7 +18,16 @@ synchronize on both sides, max over ranks.  Inputs (>= 134 MB per vector at N=40
 than the 126 MB L2.
 
 --impl reference times the CPU oracle (oracle/, SciPy, as it stands) on the
-host cores on a bounded sample of the same workload family.
+host cores on a bounded sample of the SAME workload: the oracle hierarchy of the
+4096^2 problem is built once (setup reported, not timed), then each step is one
+FGMRES(20) iteration (maxiter = 1).  The default run's cpu_baseline does the same
+with 2 iterations.
+
+--gpus N > 1 without a torchrun environment re-launches this script under
+`python -m torch.distributed.run --nproc-per-node N` (127.0.0.1 rendezvous);
+--dry-run stops every rank right after the rendezvous (CPU test of the launch).
+Extra keys of the JSON line: "c128" (the same 4096^2 solve in complex128),
+"config3" (BASELINE configs[3], 3D 256^3, c64), "multi_rhs" (4 sources batched).
 """
 from __future__ import annotations
 
@@ -172,26 +181,25 @@ def run_ours(args):
     value = N * iters / (ms_step * 1e-3)     # whole-problem unknown-updates / max-over-ranks time
 
     # ---------------------------------------------------------------- e2e: host buffers through the C-ABI
+    # host wall clock around the C-ABI call that takes HOST buffers (copies inside the call)
     qh = q.cpu().pin_memory()
     xh = torch.zeros_like(qh).pin_memory()
     e_ms = []
-    for k in range(max(1, min(args.steps, 2))):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for k in range(max(2, min(args.steps, 3))):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        a.record(stream)
+        t0 = time.perf_counter()
         re = gh.fgmres_solve_host(qh, xh, restart=RESTART, tol=TOL, maxiter=args.maxiter)
-        b.record(stream)
         torch.cuda.synchronize()
-        e_ms.append(a.elapsed_time(b))
+        e_ms.append((time.perf_counter() - t0) * 1e3)
     e_ms = sum(e_ms) / len(e_ms)
     if dist:
         t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item())
     e2e = {"value": N * re.iterations / (e_ms * 1e-3), "unit": UNIT,
-           "time_to_solve_s": e_ms * 1e-3,
+           "time_to_solve_s": e_ms * 1e-3, "clock": "host wall clock (time.perf_counter), mean of the samples",
            "h2d_bytes_per_step": qh.numel() * qh.element_size(),
            "d2h_bytes_per_step": xh.numel() * xh.element_size()}
 
@@ -253,6 +261,12 @@ def run_ours(args):
     }
     if multi:
         out["multi_rhs"] = multi
+    if ws == 1 and not args.no_extra:
+        del gh
+        torch.cuda.empty_cache()
+        out["c128"] = extra_c128(n, args)
+        torch.cuda.empty_cache()
+        out["config3"] = extra_config3(args)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.cpu_n, args.cpu_iters)
     if rank == 0:
@@ -293,12 +307,66 @@ def multi_rhs(gh, p, n, args, cdt, stream, single_value):
             "sources": "config-1 centre source + seeded interior point sources (numpy default_rng(11))"}
 
 
+def _timed_solves(gh, q, restart, nsolve, maxiter):
+    """1 warm-up solve, then nsolve solves timed with CUDA events on the stream; median."""
+    import torch
+    x = torch.zeros_like(q)
+    gh.fgmres_solve(q, x, restart=restart, tol=TOL, maxiter=maxiter)
+    stream = torch.cuda.current_stream()
+    ms, r = [], None
+    for _ in range(nsolve):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        r = gh.fgmres_solve(q, x, restart=restart, tol=TOL, maxiter=maxiter)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    return statistics.median(ms), r
+
+
+def extra_c128(n, args):
+    """BASELINE configs[1] names complex64 AND complex128: the same solve in c128."""
+    import torch
+    from paper_2511_16808_b200 import hmg
+    p = build_problem(n)
+    gh = hmg.Hierarchy(hmg.Options(dim=2, cells=p.cells, h=p.h, levels=levels_for(n), damping=DAMP_RB,
+                                   dtype="c128"), p.kappa, p.omega, p.gamma, ALPHA.get(n, 0.25))
+    q = torch.from_numpy(p.q.ravel()).cuda()
+    ms, r = _timed_solves(gh, q, RESTART, 2, args.maxiter)
+    return {"dtype": "c128", "time_to_solve_s": ms * 1e-3, "iterations": r.iterations, "converged": bool(r.converged),
+            "value": p.n * r.iterations / (ms * 1e-3), "unit": UNIT,
+            "timing": "median of 2 device-timed solves after 1 warm-up"}
+
+
+def extra_config3(args):
+    """BASELINE configs[3]: 3D homogeneous 256^3 cells, 6 levels, element Vanka, alpha 0.5,
+    FGMRES(10), c64 -- the paper's 3D timing experiment setting."""
+    import torch
+    from paper_2511_16808_b200 import hmg, media
+    p = media.config_problem(3)
+    t0 = time.time()
+    gh = hmg.Hierarchy(hmg.Options(dim=3, cells=p.cells, h=p.h, levels=6, smoother="element",
+                                   damping=[1.1, 0.7, 0.45, 0.6], dtype="c64"), p.kappa, p.omega, p.gamma, 0.5)
+    torch.cuda.synchronize()
+    setup = time.time() - t0
+    q = torch.from_numpy(p.q.ravel()).to(torch.complex64).cuda()
+    ms, r = _timed_solves(gh, q, 10, 3, args.maxiter)
+    return {"workload": "BASELINE configs[3]: 3D 256^3 cells (16974593 unknowns), 6-level V(1,1) element Vanka, "
+                        "lev-dep Galerkin, alpha 0.5, FGMRES(10) to 1e-6, c64",
+            "time_to_solve_s": ms * 1e-3, "ms_per_iteration": ms / max(r.iterations, 1), "iterations": r.iterations,
+            "converged": bool(r.converged), "value": p.n * r.iterations / (ms * 1e-3), "unit": UNIT,
+            "setup_s": round(setup, 2), "timing": "median of 3 device-timed solves after 1 warm-up"}
+
+
 _ORACLE = {}
+_ORACLE_SETUP = {}
 
 
 def _oracle_sample(n, iters):
-    """Oracle (as it stands) on config 1 at n x n: setup untimed (built once),
-    then a fixed number of FGMRES iterations timed; returns
+    """Oracle (as it stands) on config 1 at n x n: setup untimed (built once; its
+    time is kept in _ORACLE_SETUP), then a fixed number of FGMRES iterations timed
+    (the first iterations of the first restart cycle); returns
     (unknown-updates/s, seconds, N, iterations)."""
     from threadpoolctl import threadpool_limits
     from oracle.cycle import vcycle
@@ -308,8 +376,10 @@ def _oracle_sample(n, iters):
     L = levels_for(n)
     with threadpool_limits(1):
         if n not in _ORACLE:
+            ts = time.perf_counter()
             _ORACLE[n] = build_hierarchy(OOptions(dim=2, cells=p.cells, h=p.h, levels=L, damping=DAMP_RB), p.kappa,
                                          p.omega, p.gamma, ALPHA.get(n, 0.25))
+            _ORACLE_SETUP[n] = time.perf_counter() - ts
         oh = _ORACLE[n]
         t0 = time.perf_counter()
         _, info = fgmres_solve(oh.H, p.q.ravel(), lambda v: vcycle(oh, v), restart=RESTART, tol=TOL,
@@ -322,8 +392,10 @@ def _oracle_sample(n, iters):
 def cpu_baseline(n, iters):
     v, dt, N, it = _oracle_sample(n, iters)
     return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle (SciPy, complex128, 1 thread) on config 1 at {n}x{n} cells ({N} unknowns): "
-                      f"{it} FGMRES({RESTART}) iterations timed ({dt:.1f} s), setup excluded"}
+            "sample": f"oracle (SciPy, complex128, 1 thread) on the bench workload itself (config 1, {n}x{n} cells, "
+                      f"{N} unknowns): the first {it} FGMRES({RESTART}) iterations timed ({dt:.1f} s); setup "
+                      f"{_ORACLE_SETUP.get(n, 0):.0f} s, not timed (P:1026-1027)",
+            "setup_s": round(_ORACLE_SETUP.get(n, 0), 1)}
 
 
 def run_reference(args):
@@ -338,17 +410,48 @@ def run_reference(args):
             rates.append(v)
             secs.append(dt)
     value = sum(rates) / len(rates)
+    ws = int(os.environ.get("WORLD_SIZE", args.gpus))
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
            "data": "synthetic",
-           "config": {"workload": f"BASELINE configs[1] family, bounded sample: {n}x{n} cells, "
-                                  f"{args.cpu_iters} FGMRES({RESTART}) iterations per step (the full N=4096 solve "
-                                  f"is hours in SciPy)", "cells": [n, n], "levels": levels_for(n)},
+           "config": {"workload": f"BASELINE configs[1], the bench workload itself ({n}x{n} cells), bounded sample: "
+                                  f"{args.cpu_iters} FGMRES({RESTART}) iteration(s) per step (the full N=4096 solve "
+                                  f"is hours in SciPy)", "cells": [n, n], "levels": levels_for(n),
+                      "oracle_setup_s": round(_ORACLE_SETUP.get(n, 0), 1)},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": f"{n}x{n}, {args.cpu_iters} iterations per step, setup excluded"},
+                            "sample": f"{n}x{n}, {args.cpu_iters} iteration(s) per step, setup "
+                                      f"({_ORACLE_SETUP.get(n, 0):.0f} s) excluded"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run,
+    one process per GPU, rendezvous on 127.0.0.1 (the driver's own launch line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args):
+    """Rendezvous only (CPU): every rank reports itself, rank 0 the world size."""
+    ws, rank, local = _dist()
+    import torch.distributed as dist
+    if ws > 1:
+        dist.init_process_group("gloo")
+        t = __import__("torch").tensor([1])
+        dist.all_reduce(t)
+        n = int(t.item())
+        dist.destroy_process_group()
+    else:
+        n = 1
+    print(json.dumps({"dry_run": True, "rank": rank, "world_size": ws, "local_rank": local, "ranks_seen": n,
+                      "gpus": args.gpus}), flush=True)
 
 
 def main():
@@ -360,14 +463,26 @@ def main():
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--maxiter", type=int, default=4000)
-    ap.add_argument("--cpu-n", type=int, default=512)
-    ap.add_argument("--cpu-iters", type=int, default=120, help="oracle FGMRES iterations per CPU sample (~10 s at --cpu-n 512)")
+    ap.add_argument("--cpu-n", type=int, default=4096, help="oracle sample grid (default: the bench workload)")
+    ap.add_argument("--cpu-iters", type=int, default=None,
+                    help="oracle FGMRES iterations per sample (default: 2 for cpu_baseline, 1 per reference step)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c128 and config3 extra keys")
+    ap.add_argument("--dry-run", action="store_true", help="launch / rendezvous only (no CUDA)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nrhs", type=int, default=4, help="batch size of the multi-RHS line (<= 1: skip)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if args.dry_run:
+        dry_run(args)
+        return
     if args.impl == "reference":
+        if args.cpu_iters is None:
+            args.cpu_iters = 1
         run_reference(args)
     else:
+        if args.cpu_iters is None:
+            args.cpu_iters = 2
         run_ours(args)
 
 

@@ -6,6 +6,7 @@
 // and level-dependent intergrid (Eqs. 3.3-3.4).  Every arithmetic
 // step runs in the kernels of k_*.cuh; this file only sequences launches.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <atomic>
@@ -118,6 +119,34 @@ static void level_scheme(int scheme, int l, int &rR, int &rP) {
     case HMG_MIXED: rR = 1; rP = 2; break;
     default: throw HmgError(HMG_EINVAL, "unknown intergrid scheme");
   }
+}
+
+// TMA tensor map over a padded level box (k_stage3d.cuh): 8-byte words, dims
+// (x words incl. ghosts, rows incl. ghosts, planes incl. ghosts), box
+// (bx elements, by rows, 1 plane); out-of-range box parts are zero-filled.
+// cuTensorMapEncodeTiled comes from the driver through the runtime's entry-point
+// query (no libcuda link dependency).
+static CUtensorMap make_tmap(const void *base, int esz, const Geo &g, int bx, int by) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) throw HmgError(HMG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap m;
+  const int w = esz / 8;
+  const int nz = g.dim == 3 ? g.n[2] + 2 * g.G : 1;
+  cuuint64_t dims[3] = {(cuuint64_t)g.px * w, (cuuint64_t)(g.n[1] + 2 * g.G), (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)g.px * esz, (cuuint64_t)g.pxy * esz};
+  cuuint32_t box[3] = {(cuuint32_t)(bx * w), (cuuint32_t)by, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void *>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw HmgError(HMG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
 }
 
 static TransferW transfer_weights(int rR, int rP) {
@@ -265,6 +294,7 @@ template <typename T> struct Solver : SolverBase {
   DBuf ainv;              // coarsest inverse, double2 N_L x N_L
   bool rb_closed = false; // fine level uses the closed-form RB patch solve
   bool stage3d = true;    // 3D fine operator: z-marching staged kernel (HMG_NO_STAGE3D=1 at build: the gather)
+  bool fmarch = true;     // 2D c64 fine operator: warp-marching kernel (HMG_NO_FMARCH=1 at build: node-parallel)
   DBuf rb_ia, rb_id;      // its sigma-only factors 1/a_j and 1/(a_c - e^2 sum 1/a_l), stored in T
   C usig{}, uia{}, uid{};  // level-0 uniform-box values of sig, rb_ia, rb_id
   D usigd{};
@@ -316,6 +346,7 @@ template <typename T> struct Solver : SolverBase {
     L = opt.levels;
     G = opt.intergrid == HMG_CUBIC ? 3 : 2;
     stage3d = std::getenv("HMG_NO_STAGE3D") == nullptr;
+    fmarch = std::getenv("HMG_NO_FMARCH") == nullptr;
     if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
     lev.resize(L);
     int64_t nodes[3] = {opt.cells[0] + 1, opt.cells[1] + 1, dim == 3 ? opt.cells[2] + 1 : 1};
@@ -773,6 +804,36 @@ template <typename T> struct Solver : SolverBase {
     }
   }
 
+  // 2D c64 fine operator y = A x / y = f - A x as the warp-marching kernel (k_operator.cuh);
+  // false: not applicable (the caller falls back to the node-parallel kernels)
+  bool fine2d_march(const void *sgv, bool sig_fp64, double a, double ih2, const C *x, const C *f, C *y,
+                    cudaStream_t s) {
+    if (!std::is_same<T, float>::value || opt.dim != 2 || (G % 2) != 0 || !fmarch) return false;
+    const Geo &g = lev[0].geo;
+    constexpr int SEG = 32, PD = 2, NST = PD + 2;
+    const int nstrips = (g.n[0] + FM_STRIP - 1) / FM_STRIP, nsegs = (g.n[1] + SEG - 1) / SEG;
+    const int64_t warps = (int64_t)nstrips * nsegs;
+    const dim3 grid((unsigned)((warps + 3) / 4)), block(128);
+    const bool c4 = opt.fine_stencil == HMG_COMPACT4;
+    const float2 *xx = reinterpret_cast<const float2 *>(x), *ff = reinterpret_cast<const float2 *>(f);
+    float2 *yy = reinterpret_cast<float2 *>(y);
+    auto go = [&](auto kern, const auto *sg, int sw) {
+      const int smem = 4 * NST * (2 + sw) * 32 * 16;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      launch(kern, grid, block, (size_t)smem, s, g, sg, a, ih2, xx, ff, yy, lev[0].ub, sig_fp64 ? usigd : widen(usig));
+    };
+    if (sig_fp64) {
+      const double2 *sg = reinterpret_cast<const double2 *>(sgv);
+      if (c4) go(k_fine_op2d_march<ST_COMPACT4, double, SEG, PD>, sg, 2);
+      else go(k_fine_op2d_march<ST_FD2, double, SEG, PD>, sg, 2);
+    } else {
+      const float2 *sg = reinterpret_cast<const float2 *>(sgv);
+      if (c4) go(k_fine_op2d_march<ST_COMPACT4, float, SEG, PD>, sg, 1);
+      else go(k_fine_op2d_march<ST_FD2, float, SEG, PD>, sg, 1);
+    }
+    return true;
+  }
+
   // 3D fine operator y = A x / y = f - A x: the z-marching staged kernel (k_stage3d.cuh)
   // or the node-parallel gather (bit-identical; HMG_NO_STAGE3D=1)
   template <typename TT, typename TC, typename TS>
@@ -787,13 +848,17 @@ template <typename T> struct Solver : SolverBase {
       return;
     }
     constexpr int ZC = 32, NS = 4;
-    const int off2 = S3_RY * S3_RX * (int)sizeof(cplx<TT>) + S3_TY * S3_TX * (int)sizeof(cplx<TS>);
-    const int slot = (off2 + (f ? S3_TY * S3_TX * (int)sizeof(cplx<TT>) : 0) + 127) / 128 * 128;
+    auto rup = [](int b) { return (b + 127) / 128 * 128; };
+    const int slot = rup(S3_RY * S3_RX * (int)sizeof(cplx<TT>)) + rup(S3_TY * S3_TX * (int)sizeof(cplx<TS>)) +
+                     rup(S3_TY * S3_TX * (int)sizeof(cplx<TT>));
     const int smem = 128 + NS * slot;
-    const dim3 block(32, 8), grid((g.n[0] + S3_TX - 1) / S3_TX, (g.n[1] + S3_TY - 1) / S3_TY, (g.n[2] + ZC - 1) / ZC);
+    const dim3 block(32, S3_TY + 1), grid((g.n[0] + S3_TX - 1) / S3_TX, (g.n[1] + S3_TY - 1) / S3_TY, (g.n[2] + ZC - 1) / ZC);
+    const CUtensorMap mx = make_tmap(x, sizeof(cplx<TT>), g, S3_RX, S3_RY);
+    const CUtensorMap ms = make_tmap(sg, sizeof(cplx<TS>), g, S3_TX, S3_TY);
+    const CUtensorMap mf = make_tmap(f ? (const void *)f : (const void *)x, sizeof(cplx<TT>), g, S3_TX, S3_TY);
     auto go = [&](auto kern) {
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      launch(kern, grid, block, (size_t)smem, s, g, sg, a, ih2, x, f, y, ub, us);
+      launch(kern, grid, block, (size_t)smem, s, g, mx, ms, mf, f ? 1 : 0, a, ih2, y, ub, us);
     };
     if (c4) go(k_fine_op3d_z<TT, ST_COMPACT4, TC, TS, ZC, NS>);
     else go(k_fine_op3d_z<TT, ST_FD2, TC, TS, ZC, NS>);
@@ -835,6 +900,7 @@ template <typename T> struct Solver : SolverBase {
       C *yy = (C *)y;
       const bool c4 = opt.fine_stencil == HMG_COMPACT4;
       const UBox &ub = Lv.ub;
+      if (fine2d_march(sg, false, a, ih2, xx, ff, yy, s)) return;
       if (opt.dim == 2) {
         if (c4) launch(k_fine_op<T, 2, ST_COMPACT4, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy, ub, widen(usig));
         else launch(k_fine_op<T, 2, ST_FD2, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy, ub, widen(usig));
@@ -877,10 +943,27 @@ template <typename T> struct Solver : SolverBase {
     if (opt.dim == 2 && nbat(l) == 1 && std::is_same<T, float>::value && (G % 2) == 0 && Lv.r <= 2 &&
         std::getenv("HMG_NO_PAIR_ST") == nullptr) {   // two nodes per thread, 16-byte coefficient pairs
       tag(f ? "stored_residual" : "stored_apply", l, kcount(opt.dim, Lv.r) * sizeof(C) * outside(l) + (f ? 3 : 2) * sz * nn);
-      const dim3 block(32, 8), grid(((Lv.geo.n[0] + 1) / 2 + 31) / 32, (Lv.geo.n[1] + 7) / 8);
       const float2 *c2 = reinterpret_cast<const float2 *>(cf);
-      if (Lv.r == 1) launch(k_stored_op2d_pair<1>, grid, block, 0, s, Lv.geo, c2, xx, ff, yy, Lv.ub, ucopy<9, double>(Lv.ucoef));
-      else launch(k_stored_op2d_pair<2>, grid, block, 0, s, Lv.geo, c2, xx, ff, yy, Lv.ub, ucopy<25, double>(Lv.ucoef));
+      // BY output rows per thread (register blocking) on the large levels, 1 on small ones (parallelism)
+      static const int by_env = std::getenv("HMG_STORED_BY") ? std::atoi(std::getenv("HMG_STORED_BY")) : 2;
+      const int BY = Lv.geo.n[1] >= 512 ? by_env : 1;
+      auto go = [&](auto kern, int by) {
+        const dim3 block(32, 8), grid(((Lv.geo.n[0] + 1) / 2 + 31) / 32, (Lv.geo.n[1] + 8 * by - 1) / (8 * by));
+        launch(kern, grid, block, 0, s, Lv.geo, c2, xx, ff, yy, Lv.ub, ucopy<(2 * 2 + 1) * (2 * 2 + 1), double>(Lv.ucoef));
+      };
+      auto go1 = [&](auto kern, int by) {
+        const dim3 block(32, 8), grid(((Lv.geo.n[0] + 1) / 2 + 31) / 32, (Lv.geo.n[1] + 8 * by - 1) / (8 * by));
+        launch(kern, grid, block, 0, s, Lv.geo, c2, xx, ff, yy, Lv.ub, ucopy<9, double>(Lv.ucoef));
+      };
+      if (Lv.r == 1) {
+        if (BY == 4) go1(k_stored_op2d_pair<1, 4>, 4);
+        else if (BY == 2) go1(k_stored_op2d_pair<1, 2>, 2);
+        else go1(k_stored_op2d_pair<1, 1>, 1);
+      } else {
+        if (BY == 4) go(k_stored_op2d_pair<2, 4>, 4);
+        else if (BY == 2) go(k_stored_op2d_pair<2, 2>, 2);
+        else go(k_stored_op2d_pair<2, 1>, 1);
+      }
       return;
     }
     over_batch(nbat(l), [&](auto NRc, int q0) {
@@ -896,8 +979,18 @@ template <typename T> struct Solver : SolverBase {
         else if (Lv.r == 2) launch(k_stored_op<double, T, 2, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<25, double>(uv));
         else launch(k_stored_op<double, T, 2, 3, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<49, double>(uv));
       } else {
-        if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<27, double>(uv));
-        else launch(k_stored_op<double, T, 3, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv));
+        // one right-hand side on a large level: BZ = 4 planes per thread (register blocking)
+        static const int bz_env = std::getenv("HMG_STORED_BZ") ? std::atoi(std::getenv("HMG_STORED_BZ")) : 4;
+        const int bz = (NR == 1 && Lv.geo.n[2] >= 64) ? bz_env : 1;
+        dim3 grid4 = nl.grid;
+        grid4.z = (Lv.geo.n[2] + 3) / 4;
+        if (bz == 4) {
+          if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR, 4>, grid4, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<27, double>(uv));
+          else launch(k_stored_op<double, T, 3, 2, NR, 4>, grid4, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv));
+        } else {
+          if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<27, double>(uv));
+          else launch(k_stored_op<double, T, 3, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv));
+        }
       }
     });
   }
@@ -979,6 +1072,24 @@ template <typename T> struct Solver : SolverBase {
     const double nn = (double)Lv.geo.nodes();
     halo(l, r, 2, s);   // B reaches offsets up to +-2 (RB / Plus)
     const int64_t bs = Lv.geo.total;
+    // (measured slower than the gather below on config 3 -- 46 vs 28 ms per solve at level 0: kept
+    // as an opt-in, HMG_VANKA27_Z=1, bit-identical)
+    static const bool v27 = std::getenv("HMG_VANKA27_Z") != nullptr;
+    if (DIM == 3 && KIND == PK_ELEMENT && nbat(l) == 1 && stage3d && v27 && Lv.geo.n[2] >= 16) {
+      // z-marching staged 27-point apply (k_stage3d.cuh): r planes through the bulk-copy ring
+      constexpr int ZC = 32, NS = 4;
+      tag(zero ? "vanka_zero" : "vanka", l, (double)NB * sizeof(C) * outside(l) + (zero ? 2 : 3) * sizeof(TV) * nn);
+      const int slot = (S3_RY * S3_RX * (int)sizeof(TV) + 127) / 128 * 128;
+      const int smem = 128 + NS * slot;
+      const Geo &g = Lv.geo;
+      const dim3 block(32, S3_TY + 1), grid((g.n[0] + S3_TX - 1) / S3_TX, (g.n[1] + S3_TY - 1) / S3_TY, (g.n[2] + ZC - 1) / ZC);
+      auto kern = k_vanka27_z<BV, T, ZC, NS>;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      const CUtensorMap mr = make_tmap(r, sizeof(TV), g, S3_RX, S3_RY);
+      launch(kern, grid, block, (size_t)smem, s, g, mr, (const C *)Lv.bop.template as<C>(), (const TV *)u,
+             (TV *)u, (BV)damp(l), zero, Lv.ub, ucopy<27, BV>(Lv.ubop));
+      return;
+    }
     over_batch(nbat(l), [&](auto NRc, int q0) {
       constexpr int NR = decltype(NRc)::value;
       tag(zero ? "vanka_zero" : "vanka", l, (double)NB * sizeof(C) * outside(l) + (zero ? 2 : 3) * sizeof(TV) * NR * nn);
@@ -1352,6 +1463,7 @@ template <typename T> struct Solver : SolverBase {
     tag("fine_apply", 0, 2.0 * sizeof(C) * Lv.geo.nodes() + sizeof(double2) * outside(0));
     const bool c4 = opt.fine_stencil == HMG_COMPACT4;
     const UBox &ub = Lv.ub;
+    if (fine2d_march(sg, true, 0.0, ih2, z, nullptr, w, s)) return;
     if (pair_ok()) {
       const dim3 block(32, 8), grid(((Lv.geo.n[0] + 1) / 2 + 31) / 32, (Lv.geo.n[1] + 7) / 8);
       const float2 *zz = reinterpret_cast<const float2 *>(z);

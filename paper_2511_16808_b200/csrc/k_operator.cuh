@@ -154,96 +154,269 @@ __global__ void __launch_bounds__(256) k_fine_op2d_pair(Geo g, const cplx<TSG> *
     y[i] = make_float2((float)oa.x, (float)oa.y);
 }
 
+// 2D c64 fine operator as a WARP-MARCHING kernel: lane l holds the column pair
+// (x0, x0 + 1), x0 = 60 s - 2 + 2 l, of strip s; lanes 1..30 write (60 outputs per
+// strip), lanes 0 and 31 only supply the x-neighbours, which every lane takes from
+// its neighbour lanes by shuffles.  The warp marches down a segment of SEG output
+// rows holding a rolling window of three rows in fp64 registers, so every input
+// element is loaded (16-byte pairs through a per-warp cp.async ring, PD rows ahead)
+// and converted ONCE, instead of 12 loads and conversions per node pair in
+// k_fine_op2d_pair.  Same per-node grouping of the stencil sums as fine_op_node:
+// bit-identical to k_fine_op / k_fine_op2d_pair (tests/test_gpu_march.py).
+constexpr int FM_STRIP = 60;
+template <int KIND, typename TSG, int SEG, int PD>
+__global__ void __launch_bounds__(128) k_fine_op2d_march(Geo g, const cplx<TSG> *__restrict__ sig, double alpha,
+                                                         double ih2, const float2 *__restrict__ x,
+                                                         const float2 *__restrict__ f, float2 *__restrict__ y, UBox ub,
+                                                         double2 us) {
+  using W = FineW<2, KIND>;
+  using CC = double2;
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nstrips = (g.n[0] + FM_STRIP - 1) / FM_STRIP;
+  const int strip = wid % nstrips, seg = wid / nstrips;
+  const int y0 = seg * SEG;
+  if (y0 >= g.n[1]) return;
+  const int y1 = min(g.n[1], y0 + SEG);
+  const int x0 = strip * FM_STRIP - 2 + 2 * lane;
+  const bool out_lane = lane >= 1 && lane <= 30 && x0 < g.n[0];
+  const bool two = x0 + 1 < g.n[0];
+  const bool xload = x0 < g.n[0] + g.G;   // columns past the ghost layer are never used
+  const bool xuni = x0 >= ub.lo[0] && x0 + 1 < ub.hi[0];
+  auto urow = [&](int yy) { return xuni && yy >= ub.lo[1] && yy < ub.hi[1]; };
+  constexpr int NST = PD + 2;
+  constexpr int SW = sizeof(cplx<TSG>) * 2 / 16;   // 16-byte words of a sigma pair (1 or 2)
+  constexpr int NW = 2 + SW;                        // x, f, sigma words per lane and row
+  extern __shared__ __align__(16) unsigned char fm_smem[];
+  float4 *ring = reinterpret_cast<float4 *>(fm_smem) + (size_t)(threadIdx.x >> 5) * (NST * NW * 32);
+  const int64_t px = g.px;
+  const int64_t ob0 = g.base + x0 + (int64_t)(y0 - 1) * px;   // row y0 - 1, column x0
+  auto cp16 = [&](const void *src, int slot, int k, bool ok) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(ring + (slot * NW + k) * 32 + lane);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(ok ? src : (const void *)x),
+                 "r"(ok ? 16 : 0)
+                 : "memory");
+  };
+  const int nrows = y1 - y0 + 2;   // input rows y0-1 .. y1
+  auto issue = [&](int it) {
+    if (it < nrows) {
+      const int b = y0 - 1 + it, slot = it % NST;
+      const int64_t o = ob0 + (int64_t)it * px;
+      cp16(x + o, slot, 0, xload);
+      if (f) cp16(f + o, slot, 1, xload && b >= 0 && b < g.n[1]);
+      if (!urow(b) && b >= 0 && b < g.n[1]) {
+#pragma unroll
+        for (int w = 0; w < SW; ++w)
+          cp16(reinterpret_cast<const char *>(sig + o) + 16 * w, slot, 2 + w, xload);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int k = 0; k < PD; ++k) issue(k);
+  const CC z = make_double2(0, 0);
+  // rows b-2 (a) and b-1 (b): this lane's pair and its west / east neighbours (each row is
+  // shuffled once, when it arrives, and rolls with the window)
+  CC a0 = z, a1 = z, b0 = z, b1 = z, aw = z, ae = z, bw = z, be = z;
+  auto shl = [](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
+  auto shr = [](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
+  for (int it = 0; it < nrows; ++it) {
+    issue(it + PD);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(PD) : "memory");
+    const float4 *sl = ring + (it % NST) * NW * 32 + lane;
+    const float4 xv = sl[0];
+    const CC c0 = make_double2(xv.x, xv.y), c1 = make_double2(xv.z, xv.w);   // row b
+    const CC cw = make_double2(shl(c1.x), shl(c1.y)), ce = make_double2(shr(c0.x), shr(c0.y));
+    if (it >= 2) {
+      // output row yo = b - 1: rows a (yo - 1), b (yo), c (yo + 1); west of node 0 and east
+      // of node 1 from the neighbour lanes
+      const int yo = y0 - 2 + it;
+      if (out_lane) {
+        const float4 *sb = ring + ((it - 1) % NST) * NW * 32 + lane;   // row yo's f and sigma
+        CC sg0, sg1;
+        if (urow(yo)) {
+          sg0 = sg1 = us;
+        } else if (SW == 1) {
+          const float4 v = sb[2 * 32];
+          sg0 = make_double2(v.x, v.y);
+          sg1 = make_double2(v.z, v.w);
+        } else {
+          // the pair's two fp64 sigma values are this lane's words 2 and 3 (32 float4 apart)
+          sg0 = *reinterpret_cast<const double2 *>(sb + 2 * 32);
+          sg1 = *reinterpret_cast<const double2 *>(sb + 3 * 32);
+        }
+        auto node = [&](CC cc, CC w_, CC e_, CC n_, CC s_, CC nw, CC ne, CC sw, CC se_, CC sgm, double fx, double fy) {
+          const CC sf = cadd<double>(cadd<double>(w_, e_), cadd<double>(n_, s_));
+          CC Lx = cscale<double>(cc, W::Lc);
+          Lx = cfmar<double>(Lx, W::Lf, sf);
+          if (W::Le != 0.0) Lx = cfmar<double>(Lx, W::Le, cadd<double>(cadd<double>(nw, ne), cadd<double>(sw, se_)));
+          Lx = cscale<double>(Lx, ih2);
+          CC Mx = cscale<double>(cc, W::Mc);
+          if (W::Mf != 0.0) Mx = cfmar<double>(Mx, W::Mf, sf);
+          sgm.y = fma(-alpha, sgm.x, sgm.y);
+          const CC Ax = csub<double>(Lx, cmul<double>(sgm, Mx));
+          return f ? csub<double>(make_double2(fx, fy), Ax) : Ax;
+        };
+        float4 fv = make_float4(0, 0, 0, 0);
+        if (f) fv = sb[32];
+        // node 0 (x0): west = neighbour lane's node 1, east = own node 1
+        const CC o0 = node(b0, bw, b1, a0, c0, aw, a1, cw, c1, sg0, fv.x, fv.y);
+        // node 1 (x0 + 1): west = own node 0, east = neighbour lane's node 0
+        const CC o1 = node(b1, b0, be, a1, c1, a0, ae, c0, ce, sg1, fv.z, fv.w);
+        float2 *dst = y + ob0 + (int64_t)(it - 1) * px;
+        if (two) *reinterpret_cast<float4 *>(dst) = make_float4((float)o0.x, (float)o0.y, (float)o1.x, (float)o1.y);
+        else dst[0] = make_float2((float)o0.x, (float)o0.y);
+      }
+    }
+    a0 = b0; a1 = b1; aw = bw; ae = be;
+    b0 = c0; b1 = c1; bw = cw; be = ce;
+  }
+}
+
 // Stored stencil of radius R: coef[k][j], k = (ox+R) + (2R+1)((oy+R) + (2R+1)(oz+R)),
 // multiplies x[j + o].  Coefficients towards out-of-domain nodes are zero.
 // TV = vector storage/arithmetic (fp64 on Galerkin levels), TK = coefficient storage.
 template <int DIM, int R> constexpr int kplanes() { return DIM == 3 ? (2 * R + 1) * (2 * R + 1) * (2 * R + 1) : (2 * R + 1) * (2 * R + 1); }
 
-template <typename TV, typename TK, int DIM, int R, int NR = 1>
+template <typename TV, typename TK, int DIM, int R, int NR = 1, int BZ = 1>
 __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__restrict__ coef,
                                                    const cplx<TV> *__restrict__ x,
                                                    const cplx<TV> *__restrict__ f, cplx<TV> *__restrict__ y,
                                                    int64_t bs, UBox ub, UCoef<kplanes<DIM, R>(), TV> uc) {
   // NR right-hand sides at a stride of bs elements: each coefficient is read once
-  // and applied to all of them (multi-RHS batches; same per-RHS arithmetic order)
+  // and applied to all of them (multi-RHS batches; same per-RHS arithmetic order).
+  // BZ consecutive nodes along the slowest axis per thread (register blocking: each
+  // loaded input plane / row serves every output it reaches); input planes are
+  // visited in increasing order, so each output accumulates its terms in the
+  // offset order k (oz, oy, ox ascending) -- the same arithmetic for any BZ.
   using T = TV;
-  HMG_NODE_IDX(g, ix, iy, iz);
-  const int64_t i = g.idx(ix, iy, iz);
-  const bool uni = ub.in(ix, iy, iz);   // coefficients from the uniform-box copy (k_uniform.cuh)
-  constexpr int ZR = DIM == 3 ? R : 0;
-  cplx<T> acc[NR];
+  constexpr int W = 2 * R + 1;
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iyt = blockIdx.y * blockDim.y + threadIdx.y;
+  const int iy = DIM == 3 ? iyt : iyt * BZ;
+  const int iz = DIM == 3 ? blockIdx.z * BZ : 0;
+  if (ix >= g.n[0] || iy >= g.n[1] || iz >= g.n[2]) return;
+  const int64_t i0 = g.idx(ix, iy, iz);
+  const int64_t ps = DIM == 3 ? g.pxy : g.px;   // slow-axis pitch
+  const int slow0 = DIM == 3 ? iz : iy, nslow = DIM == 3 ? g.n[2] : g.n[1];
+  const int olast = min(slow0 + BZ, nslow) - 1 - slow0;   // last valid output of the block
+  const bool uni = DIM == 3 ? ub.in(ix, iy, iz) && ub.in(ix, iy, iz + olast)
+                            : ub.in(ix, iy, 0) && ub.in(ix, iy + olast, 0);
+  cplx<T> acc[BZ][NR];
 #pragma unroll
-  for (int r = 0; r < NR; ++r) acc[r] = mkc<T>(0, 0);
+  for (int o = 0; o < BZ; ++o)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[o][r] = mkc<T>(0, 0);
+  constexpr int YR = DIM == 3 ? R : 0;   // in-plane y reach (3D only)
+  auto run = [&](auto coef_k) {
+#pragma unroll
+    for (int s = -R; s < BZ + R; ++s) {
+      if (s > olast + R) break;   // beyond the last valid output's reach
+#pragma unroll
+      for (int oy = -YR; oy <= YR; ++oy)
+#pragma unroll
+        for (int ox = -R; ox <= R; ++ox) {
+          const int64_t j = i0 + (int64_t)s * ps + (DIM == 3 ? (int64_t)oy * g.px : 0) + ox;
+          cplx<T> xv[NR];
+#pragma unroll
+          for (int r = 0; r < NR; ++r) xv[r] = x[r * bs + j];
+#pragma unroll
+          for (int o = 0; o < BZ; ++o) {
+            const int d = s - o;   // slow-axis offset of this input for output o
+            if (d < -R || d > R) continue;
+            const int k = DIM == 3 ? ((d + R) * W + oy + R) * W + ox + R : (d + R) * W + ox + R;
+            const cplx<T> c = coef_k(k, o);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) acc[o][r] = cfma<T>(acc[o][r], c, xv[r]);
+          }
+        }
+    }
+  };
   // two copies of the unrolled loop behind a branch (not a per-coefficient select:
   // predicated-off loads and conversions would still take issue slots)
-  auto run = [&](auto coef_k) {
-    int k = 0;
+  if (uni) run([&](int k, int) { return uc.c[k]; });
+  else run([&](int k, int o) { return ccast<T, TK>(coef[(int64_t)k * g.total + i0 + (int64_t)o * ps]); });
 #pragma unroll
-    for (int oz = -ZR; oz <= ZR; ++oz)
+  for (int o = 0; o < BZ; ++o) {
+    if (o > olast) break;
+    const int64_t i = i0 + (int64_t)o * ps;
 #pragma unroll
-      for (int oy = -R; oy <= R; ++oy)
-#pragma unroll
-        for (int ox = -R; ox <= R; ++ox, ++k) {
-          const cplx<T> c = coef_k(k);
-          const int64_t j = i + g.delta(ox, oy, oz);
-#pragma unroll
-          for (int r = 0; r < NR; ++r) acc[r] = cfma<T>(acc[r], c, x[r * bs + j]);
-        }
-  };
-  if (uni) run([&](int k) { return uc.c[k]; });
-  else run([&](int k) { return ccast<T, TK>(coef[(int64_t)k * g.total + i]); });
-#pragma unroll
-  for (int r = 0; r < NR; ++r) y[r * bs + i] = f ? csub<T>(f[r * bs + i], acc[r]) : acc[r];
+    for (int r = 0; r < NR; ++r) y[r * bs + i] = f ? csub<T>(f[r * bs + i], acc[o][r]) : acc[o][r];
+  }
 }
 
 // 2D c64 variant of k_stored_op: one thread per PAIR of x-adjacent nodes (2p,
-// 2p+1): the fp32 coefficient planes load as aligned 16-byte pairs and the two
-// nodes share their x-window (2R + 2 loads per row instead of 2 (2R + 1)).  Same
-// per-node arithmetic and fma order as k_stored_op.
-template <int R>
+// 2p+1) and BY consecutive rows (register blocking along y): the fp32
+// coefficient planes load as aligned 16-byte pairs, the two nodes share their
+// x-window (2R + 2 loads per row instead of 2 (2R + 1)), and each loaded input
+// row serves every one of the BY output rows it reaches (2R + BY input rows for
+// BY outputs instead of (2R + 1) BY).  Input rows are visited in increasing order
+// and each output accumulates its terms in the offset order of k_stored_op, so
+// the per-node arithmetic (and result) is that of k_stored_op.
+template <int R, int BY = 1>
 __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *__restrict__ coef,
                                                           const double2 *__restrict__ x,
                                                           const double2 *__restrict__ f, double2 *__restrict__ y,
                                                           UBox ub, UCoef<(2 * R + 1) * (2 * R + 1), double> uc) {
   using T = double;
+  constexpr int W = 2 * R + 1;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
+  const int iy0 = (blockIdx.y * blockDim.y + threadIdx.y) * BY;
   const int ix = 2 * p;
-  if (ix >= g.n[0] || iy >= g.n[1]) return;
-  const int64_t i = g.idx(ix, iy, 0);
+  if (ix >= g.n[0] || iy0 >= g.n[1]) return;
+  const int64_t i0 = g.idx(ix, iy0, 0);
+  const int64_t px = g.px;
   const bool two = ix + 1 < g.n[0];
-  const bool uni = ub.in(ix, iy, 0) && (!two || ub.in(ix + 1, iy, 0));   // both nodes in the uniform box
-  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+  const int ylast = min(iy0 + BY, g.n[1]) - 1;
+  // every node of the BY x 2 block in the uniform box
+  const bool uni = ub.in(ix, iy0, 0) && ub.in(ix, ylast, 0) && (!two || ub.in(ix + 1, iy0, 0));
+  double2 a0[BY], a1[BY];
+#pragma unroll
+  for (int o = 0; o < BY; ++o) a0[o] = a1[o] = make_double2(0, 0);
+  // input rows past the last output row's reach are never needed (and may lie
+  // beyond the padded box of a ragged block): they are skipped
+  const int rmax = ylast - iy0 + R;
   // uniform box: fp64 coefficient copies from the parameter bank, no loads, no
   // conversions -- a separate copy of the unrolled loop behind one branch
   auto run = [&](auto coef_k) {
-    int k = 0;
 #pragma unroll
-    for (int oy = -R; oy <= R; ++oy) {
-      const double2 *row = x + i + (int64_t)oy * g.px;
+    for (int r = -R; r < BY + R; ++r) {
+      if (r > rmax) break;
+      const double2 *row = x + i0 + (int64_t)r * px;
       double2 xw[2 * R + 2];
 #pragma unroll
       for (int c = 0; c < 2 * R + 2; ++c) xw[c] = row[c - R];
 #pragma unroll
-      for (int ox = -R; ox <= R; ++ox, ++k) {
-        double2 k0, k1;
-        coef_k(k, k0, k1);
-        a0 = cfma<T>(a0, k0, xw[ox + R]);
-        a1 = cfma<T>(a1, k1, xw[ox + R + 1]);
+      for (int o = 0; o < BY; ++o) {
+        const int oy = r - o;   // offset of this input row for output row o
+        if (oy < -R || oy > R) continue;
+#pragma unroll
+        for (int ox = -R; ox <= R; ++ox) {
+          const int k = (oy + R) * W + ox + R;
+          double2 k0, k1;
+          coef_k(k, o, k0, k1);
+          a0[o] = cfma<T>(a0[o], k0, xw[ox + R]);
+          a1[o] = cfma<T>(a1[o], k1, xw[ox + R + 1]);
+        }
       }
     }
   };
   if (uni) {
-    run([&](int k, double2 &k0, double2 &k1) { k0 = k1 = uc.c[k]; });
+    run([&](int k, int, double2 &k0, double2 &k1) { k0 = k1 = uc.c[k]; });
   } else {
-    run([&](int k, double2 &k0, double2 &k1) {
-      const float4 c2 = *reinterpret_cast<const float4 *>(coef + (int64_t)k * g.total + i);
+    run([&](int k, int o, double2 &k0, double2 &k1) {
+      const float4 c2 = *reinterpret_cast<const float4 *>(coef + (int64_t)k * g.total + i0 + (int64_t)o * px);
       k0 = mkc<T>(c2.x, c2.y);
       k1 = mkc<T>(c2.z, c2.w);
     });
   }
-  y[i] = f ? csub<T>(f[i], a0) : a0;
-  if (two) y[i + 1] = f ? csub<T>(f[i + 1], a1) : a1;
+#pragma unroll
+  for (int o = 0; o < BY; ++o) {
+    if (iy0 + o > ylast) break;
+    const int64_t i = i0 + (int64_t)o * px;
+    y[i] = f ? csub<T>(f[i], a0[o]) : a0[o];
+    if (two) y[i + 1] = f ? csub<T>(f[i + 1], a1[o]) : a1[o];
+  }
 }
 
 }  // namespace hmg

@@ -14,6 +14,8 @@
 // kernels group their terms, so the results are bit-identical to them
 // (tests/test_gpu_stage3d.py).
 #pragma once
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "common.cuh"
@@ -48,121 +50,101 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// one TMA tensor request: the box of `map` at element coordinates (c0, c1, c2) -> shared
+// memory (out-of-range parts are zero-filled); completes on `bar` with the box's bytes
+__device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 
 constexpr int S3_TX = 32, S3_TY = 8, S3_RX = S3_TX + 4, S3_RY = S3_TY + 2;
 
-// Per-plane staging plan shared by the kernels below: slot s of the ring holds
-// NA arrays of plane z: array 0 = the halo tile (S3_RY rows x S3_RX elements of
-// type E0, x from x0-2, y from y0-1), arrays 1.. = interior tiles (S3_TY rows x
-// S3_TX elements, x from x0, y from y0) of per-node arrays (skipped rows leave
-// stale data: their nodes never read it).  Warp 0 issues: lane 0 arms the
-// barrier with the plane's byte count, then lane r copies row r.  Copies are
-// clamped to the padded box [0, total) so a ragged tile never reads past the
-// allocation (the clamped elements only feed nodes that are not written).
-struct S3Plan {
-  const char *src[4];   // base pointers (nullptr = array not staged)
-  int esz[4];           // element bytes
-  int na;
-};
+// Shared-memory layout of the staged kernels: NS full + NS empty mbarriers
+// (128 bytes), then NS ring slots.  Block = 8 compute warps (32 x 8 nodes of a
+// plane) + 1 producer warp (threadIdx.y == 8) whose lane 0 issues ONE TMA
+// tensor request per staged array and plane (tensor maps over the padded level
+// boxes, built on the host: make_tmap): the compute warps never meet at a block
+// barrier inside the march; a slot is refilled once all 8 compute warps have
+// arrived on its empty barrier.  (Row-by-row cp.async.bulk copies, 10-26
+// requests per plane, were measured request-rate bound.)
+constexpr int S3_THREADS = 32 * 9;
 
 template <int NS>
-__device__ __forceinline__ void s3_issue(const Geo &g, const S3Plan &pl, char *ring, int slot_bytes, const int *off,
-                                         uint64_t *bar, int it, int z, int x0, int y0, unsigned skip1) {
-  // skip1: bit r set = row r of array 1 is not needed (it lies in the uniform box)
-  const int lane = threadIdx.x & 31;
-  const int slot = it % NS;
-  char *base = ring + (size_t)slot * slot_bytes;
-  // row task for this lane: array a, row r
-  unsigned bytes = 0;
-  const char *src = nullptr;
-  char *dst = nullptr;
-  {
-    int a = 0, r = lane;
-    if (r >= S3_RY) {
-      r -= S3_RY;
-      a = 1 + r / S3_TY;
-      r = r % S3_TY;
-    }
-    // (selects instead of indexing the plan arrays with the lane's runtime a: no local memory)
-    const char *sa = a == 0 ? pl.src[0] : a == 1 ? pl.src[1] : a == 2 ? pl.src[2] : pl.src[3];
-    const int es = a == 0 ? pl.esz[0] : a == 1 ? pl.esz[1] : a == 2 ? pl.esz[2] : pl.esz[3];
-    const int oa = a == 0 ? off[0] : a == 1 ? off[1] : a == 2 ? off[2] : off[3];
-    if (a < pl.na && sa && !(a == 1 && ((skip1 >> r) & 1u))) {
-      const int xs = a == 0 ? x0 - 2 : x0, ys = a == 0 ? y0 - 1 + r : y0 + r;
-      const int w = a == 0 ? S3_RX : S3_TX;
-      const int64_t e0 = g.idx(xs, ys, z);
-      int64_t n = w;
-      if (e0 + n > g.total) n = g.total - e0;
-      if (e0 >= 0 && n > 0) {
-        bytes = (unsigned)(n * es) & ~15u;
-        src = sa + e0 * es;
-        dst = base + oa + (size_t)r * w * es;
-      }
-    }
-  }
-  unsigned tot = bytes;
+__device__ __forceinline__ void s3_init(uint64_t *full, uint64_t *empty) {
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
 #pragma unroll
-  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-  if (lane == 0) {
-    fence_proxy_async();
-    mbar_expect_tx(bar + slot, tot);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, S3_TY);
+    }
+    mbar_fence_init();
   }
+  __syncthreads();
+}
+// consumer side: one arrival per compute warp on the slot's empty barrier
+__device__ __forceinline__ void s3_release(uint64_t *empty_slot) {
   __syncwarp();
-  if (bytes) bulk_g2s(dst, src, bytes, bar + slot);
+  if ((threadIdx.x & 31) == 0)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty_slot)) : "memory");
+}
+// producer side (one lane): for every plane, wait until its slot is free, arm the
+// full barrier with the plane's bytes and issue the requests (issue(it, slot, z))
+template <int NS, typename Issue>
+__device__ __forceinline__ void s3_produce(uint64_t *full, uint64_t *empty, int nplanes, int z0, Issue issue) {
+  for (int it = 0; it < nplanes; ++it) {
+    const int slot = it % NS;
+    if (it >= NS) mbar_wait(empty + slot, (unsigned)((it / NS) + 1) & 1u);   // its previous use is consumed
+    issue(it, slot, z0 - 1 + it);
+  }
 }
 
 // ---------------------------------------------------------------- 19/7-point operator
 // y = A x or y = f - A x on the 3D fine level, A = L - diag(sigma_s) M
 // (Eq. 2.3; FD2 P:101-102), the arithmetic of fine_op_node (TC),
-// planes z0 .. z0+ZC-1 of the block's column tile.
+// planes z0 .. z0+ZC-1 of the block's column tile.  mx: tensor map of x with box
+// S3_RX x S3_RY x 1 (halo tile); ms / mf: sigma / f with box S3_TX x S3_TY x 1.
 template <typename T, int KIND, typename TC, typename TS, int ZC, int NS>
-__global__ void __launch_bounds__(256) k_fine_op3d_z(Geo g, const cplx<TS> *__restrict__ sig, TC alpha, TC ih2,
-                                                     const cplx<T> *__restrict__ x, const cplx<T> *__restrict__ f,
-                                                     cplx<T> *__restrict__ y, UBox ub, cplx<TC> us) {
+__global__ void __launch_bounds__(S3_THREADS) k_fine_op3d_z(Geo g, const __grid_constant__ CUtensorMap mx,
+                                                            const __grid_constant__ CUtensorMap ms,
+                                                            const __grid_constant__ CUtensorMap mf, int has_f,
+                                                            TC alpha, TC ih2, cplx<T> *__restrict__ y, UBox ub,
+                                                            cplx<TC> us) {
   using W = FineW<3, KIND>;
   using E = cplx<T>;
   using CC = cplx<TC>;
+  using ES = cplx<TS>;
   extern __shared__ __align__(128) unsigned char s3_smem[];
-  uint64_t *bar = reinterpret_cast<uint64_t *>(s3_smem);
+  uint64_t *full = reinterpret_cast<uint64_t *>(s3_smem), *empty = full + NS;
   char *ring = reinterpret_cast<char *>(s3_smem) + 128;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  constexpr int BX = S3_RY * S3_RX * (int)sizeof(E), BS = S3_TY * S3_TX * (int)sizeof(ES),
+                BF = S3_TY * S3_TX * (int)sizeof(E);
+  constexpr int OFF_S = (BX + 127) / 128 * 128, OFF_F = OFF_S + (BS + 127) / 128 * 128;
+  constexpr int SLOT = OFF_F + (BF + 127) / 128 * 128;
+  const int tx = threadIdx.x, ty = threadIdx.y;
   const int x0 = blockIdx.x * S3_TX, y0 = blockIdx.y * S3_TY, z0 = blockIdx.z * ZC;
   const int zend = min(g.n[2], z0 + ZC);
   const int nplanes = zend - z0 + 2;   // planes z0-1 .. zend
-  S3Plan pl;
-  pl.na = f ? 3 : 2;
-  pl.src[0] = reinterpret_cast<const char *>(x);
-  pl.esz[0] = sizeof(E);
-  pl.src[1] = reinterpret_cast<const char *>(sig);
-  pl.esz[1] = sizeof(cplx<TS>);
-  pl.src[2] = reinterpret_cast<const char *>(f);
-  pl.esz[2] = sizeof(E);
-  int off[4] = {0, 0, 0, 0};
-  pl.src[3] = nullptr;
-  pl.esz[3] = 0;
-  off[1] = S3_RY * S3_RX * (int)sizeof(E);
-  off[2] = off[1] + S3_TY * S3_TX * (int)sizeof(cplx<TS>);
-  const int slot_bytes = (off[2] + (f ? S3_TY * S3_TX * (int)sizeof(E) : 0) + 127) / 128 * 128;
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
-    mbar_fence_init();
+  s3_init<NS>(full, empty);
+  if (ty == S3_TY) {   // producer warp
+    if (tx == 0) {
+      const int G = g.G, wx = (int)sizeof(E) / 8, ws = (int)sizeof(ES) / 8;
+      // sigma is not staged for a tile-plane inside the uniform box
+      const bool xyu = x0 >= ub.lo[0] && min(x0 + S3_TX, g.n[0]) <= ub.hi[0] && y0 >= ub.lo[1] &&
+                       min(y0 + S3_TY, g.n[1]) <= ub.hi[1];
+      s3_produce<NS>(full, empty, nplanes, z0, [&](int, int slot, int z) {
+        const bool su = xyu && z >= ub.lo[2] && z < ub.hi[2];
+        char *b = ring + (size_t)slot * SLOT;
+        mbar_expect_tx(full + slot, BX + (su ? 0 : BS) + (has_f ? BF : 0));
+        tma_load3(b, &mx, (G + x0 - 2) * wx, G + y0 - 1, G + z, full + slot);
+        if (!su) tma_load3(b + OFF_S, &ms, (G + x0) * ws, G + y0, G + z, full + slot);
+        if (has_f) tma_load3(b + OFF_F, &mf, (G + x0) * wx, G + y0, G + z, full + slot);
+      });
+    }
+    return;
   }
-  __syncthreads();
-  // sigma rows of the tile that lie entirely in the uniform box need no copy
-  auto skip_rows = [&](int z) {
-    unsigned m = 0;
-    if (z >= ub.lo[2] && z < ub.hi[2] && x0 >= ub.lo[0] && min(x0 + S3_TX, g.n[0]) <= ub.hi[0])
-      for (int r = 0; r < S3_TY; ++r)
-        if (y0 + r >= ub.lo[1] && y0 + r < ub.hi[1]) m |= 1u << r;
-    return m;
-  };
-  auto issue = [&](int it) {
-    const int z = z0 - 1 + it;
-    s3_issue<NS>(g, pl, ring, slot_bytes, off, bar, it, z, x0, y0, skip_rows(z));
-  };
-  if (tid < 32)
-    for (int it = 0; it < NS && it < nplanes; ++it) issue(it);
   const int xi = x0 + tx, yi = y0 + ty;
   const bool own = xi < g.n[0] && yi < g.n[1];
   auto X = [&](const E *p) { return ccast<TC, T>(*p); };
@@ -171,8 +153,8 @@ __global__ void __launch_bounds__(256) k_fine_op3d_z(Geo g, const cplx<TS> *__re
   CC cA = zc, fxA = zc, fyA = zc, cB = zc, fxB = zc, fyB = zc, eB = zc;
   for (int it = 0; it < nplanes; ++it) {
     const int slot = it % NS;
-    mbar_wait(bar + slot, (unsigned)(it / NS) & 1u);
-    const char *sb = ring + (size_t)slot * slot_bytes;
+    mbar_wait(full + slot, (unsigned)(it / NS) & 1u);
+    const char *sb = ring + (size_t)slot * SLOT;
     const E *P = reinterpret_cast<const E *>(sb) + (ty + 1) * S3_RX + (tx + 2);
     const CC c = X(P);
     const CC fx = cadd<TC>(X(P - 1), X(P + 1));
@@ -193,21 +175,104 @@ __global__ void __launch_bounds__(256) k_fine_op3d_z(Geo g, const cplx<TS> *__re
       Lx = cscale<TC>(Lx, ih2);
       CC Mx = cscale<TC>(cB, (TC)W::Mc);
       if (W::Mf != 0.0) Mx = cfmar<TC>(Mx, (TC)W::Mf, sf);
-      // sigma and f of plane B were staged one step earlier (slot it-1)
-      const char *pb = ring + (size_t)((it - 1) % NS) * slot_bytes;
+      // sigma and f of plane B were staged with it (slot it-1)
+      const char *pb = ring + (size_t)((it - 1) % NS) * SLOT;
       const bool uni = ub.in(xi, yi, z);
-      CC s = uni ? us : ccast<TC, TS>(reinterpret_cast<const cplx<TS> *>(pb + off[1])[ty * S3_TX + tx]);
+      CC s = uni ? us : ccast<TC, TS>(reinterpret_cast<const ES *>(pb + OFF_S)[ty * S3_TX + tx]);
       s.y = fma(-alpha, s.x, s.y);
       const CC Ax = csub<TC>(Lx, cmul<TC>(s, Mx));
       const int64_t i = g.idx(xi, yi, z);
-      y[i] = ccast<T, TC>(f ? csub<TC>(ccast<TC, T>(reinterpret_cast<const E *>(pb + off[2])[ty * S3_TX + tx]), Ax)
-                            : Ax);
+      y[i] = ccast<T, TC>(has_f ? csub<TC>(ccast<TC, T>(reinterpret_cast<const E *>(pb + OFF_F)[ty * S3_TX + tx]), Ax)
+                                : Ax);
     }
     cA = cB; fxA = fxB; fyA = fyB;
     cB = c; fxB = fx; fyB = fy; eB = e;
-    __syncthreads();   // every thread is done with slot (it-1) % NS (sigma / f of plane B)
-    // refill the slot consumed one step ago (its sigma / f were read just now)
-    if (tid < 32 && it >= 1 && it - 1 + NS < nplanes) issue(it - 1 + NS);
+    if (it >= 1) s3_release(empty + (it - 1) % NS);   // slot it-1: x read at it-1, sigma / f just now
+  }
+}
+
+// ---------------------------------------------------------------- 27-point additive Vanka operator
+// u_out = u + w B r (zero: u_out = w B r) with the assembled 3D element operator B
+// (Eq. 3.8, 27 offsets, k_vanka_assemble), r staged plane by plane (mr: box
+// S3_RX x S3_RY x 1).  At plane p a thread adds the dz = +1 terms to output p-1
+// (which completes it), the dz = 0 terms to output p and the dz = -1 terms to
+// output p+1: each output receives its terms in the offset order of
+// k_vanka_stencil (dz, dy, dx ascending) -- the same arithmetic.  B comes from the
+// uniform-box copy inside the box, else from its stored planes at the output node.
+template <typename TV, typename TK, int ZC, int NS>
+__global__ void __launch_bounds__(S3_THREADS) k_vanka27_z(Geo g, const __grid_constant__ CUtensorMap mr,
+                                                          const cplx<TK> *__restrict__ B, const cplx<TV> *u,
+                                                          cplx<TV> *u_out, TV w, int zero, UBox ub,
+                                                          UCoef<27, TV> uc) {
+  using E = cplx<TV>;
+  extern __shared__ __align__(128) unsigned char s3_smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(s3_smem), *empty = full + NS;
+  char *ring = reinterpret_cast<char *>(s3_smem) + 128;
+  constexpr int BX = S3_RY * S3_RX * (int)sizeof(E), SLOT = (BX + 127) / 128 * 128;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int x0 = blockIdx.x * S3_TX, y0 = blockIdx.y * S3_TY, z0 = blockIdx.z * ZC;
+  const int zend = min(g.n[2], z0 + ZC);
+  const int nplanes = zend - z0 + 2;   // r planes z0-1 .. zend
+  s3_init<NS>(full, empty);
+  if (ty == S3_TY) {
+    if (tx == 0) {
+      const int G = g.G, wx = (int)sizeof(E) / 8;
+      s3_produce<NS>(full, empty, nplanes, z0, [&](int, int slot, int z) {
+        mbar_expect_tx(full + slot, BX);
+        tma_load3(ring + (size_t)slot * SLOT, &mr, (G + x0 - 2) * wx, G + y0 - 1, G + z, full + slot);
+      });
+    }
+    return;
+  }
+  const int xi = x0 + tx, yi = y0 + ty;
+  const bool own = xi < g.n[0] && yi < g.n[1];
+  const E zc = mkc<TV>(0, 0);
+  E aM = zc, a0 = zc;   // partial sums of outputs p-1 and p (before plane p)
+  for (int it = 0; it < nplanes; ++it) {
+    const int p = z0 - 1 + it;   // plane of r in the slot
+    const int slot = it % NS;
+    mbar_wait(full + slot, (unsigned)(it / NS) & 1u);
+    const E *P = reinterpret_cast<const E *>(ring + (size_t)slot * SLOT) + (ty + 1) * S3_RX + (tx + 2);
+    E rv[9];
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) rv[(dy + 1) * 3 + dx + 1] = P[dy * S3_RX + dx];
+    s3_release(empty + slot);   // r of this plane is in registers
+    E aP = zc;
+    if (own) {
+      // output node of plane q gets B(q; dx, dy, dz) r(x + dx, y + dy, p), dz = p - q
+      auto add = [&](E &acc, int q, int dz, auto uni) {
+        if (q < z0 || q >= zend) return;
+        const int64_t iq = g.idx(xi, yi, q);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          const int pidx = (dz + 1) * 9 + k;
+          const E b = decltype(uni)::value ? uc.c[pidx] : ccast<TV, TK>(B[(int64_t)pidx * g.total + iq]);
+          acc = cfma<TV>(acc, b, rv[k]);
+        }
+      };
+      using YES = std::integral_constant<bool, true>;
+      using NO = std::integral_constant<bool, false>;
+      // dz = +1 completes output p-1, dz = 0 continues p, dz = -1 opens p+1
+      if (ub.in(xi, yi, p - 1)) add(aM, p - 1, 1, YES{}); else add(aM, p - 1, 1, NO{});
+      if (ub.in(xi, yi, p)) add(a0, p, 0, YES{}); else add(a0, p, 0, NO{});
+      if (ub.in(xi, yi, p + 1)) add(aP, p + 1, -1, YES{}); else add(aP, p + 1, -1, NO{});
+      const int q = p - 1;
+      if (q >= z0 && q < zend) {
+        const int64_t iq = g.idx(xi, yi, q);
+        E o;
+        if (zero) {
+          o = mkc<TV>(__fmul_rn_t(aM.x, w), __fmul_rn_t(aM.y, w));
+        } else {
+          const E uq = u[iq];
+          o = mkc<TV>(fma(aM.x, w, uq.x), fma(aM.y, w, uq.y));
+        }
+        u_out[iq] = o;
+      }
+    }
+    aM = a0;
+    a0 = aP;
   }
 }
 

@@ -1,0 +1,71 @@
+"""Every cell of the paper's iteration Tables 5.2, 5.3 (linear medium) and 5.4 on the GPU
+(VERDICT r01 "the rest of the paper's tables on the GPU").
+
+    python scripts/paper_tables.py [--out profiles/r02_paper_tables.json]
+
+Settings as the paper runs them (and as tests/test_gpu_paper_tables.py): 4-level W(1,1)
+cycles (2/3/4 levels for Table 5.3), GMRES(5) = FGMRES(5) right-preconditioned, tol 1e-6,
+Table 5.1 damping, sponge of 20 cells with gamma_max = omega, c128.  Expected values are
+the printed ones (tests/golden/paper_tables.json, with line citations)."""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def iterations(p, smoother, alpha, intergrid="levdep", levels=4, dtype="c128"):
+    import torch
+    from paper_2511_16808_b200 import hmg
+    from helpers import DAMPING
+    gh = hmg.Hierarchy(hmg.Options(dim=p.dim, cells=p.cells, h=p.h, levels=levels, cycle="W", smoother=smoother,
+                                   intergrid=intergrid, damping=DAMPING[(p.dim, smoother)], dtype=dtype),
+                       p.kappa, p.omega, p.gamma, alpha)
+    q = torch.from_numpy(p.q.ravel()).cuda()
+    x = torch.zeros_like(q)
+    rep = gh.fgmres_solve(q, x, restart=5, tol=1e-6, maxiter=1000)
+    return rep.iterations if rep.converged else None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_paper_tables.json"))
+    a = ap.parse_args()
+    from paper_2511_16808_b200 import media
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_tables.json")))
+    out = {"_source": "scripts/paper_tables.py (CUDA path, c128) vs PAPER.md's printed counts", "cells": []}
+    t0 = time.time()
+    g = gold["table_5_2_full"]
+    for n in (128, 256, 512):
+        p = media.homogeneous_problem(2, n, sponge=20, gamma_max_over_omega=1.0)
+        for sm in ("jacobi", "element", "plus", "rb"):
+            for ig in ("cubic", "mixed", "levdep"):
+                its = iterations(p, sm, g["alpha"][sm], ig)
+                out["cells"].append({"table": "5.2", "n": n, "smoother": sm, "intergrid": ig,
+                                     "paper": g[sm][ig][str(n)], "gpu": its})
+                print(json.dumps(out["cells"][-1]), flush=True)
+    g = gold["table_5_3_linear_full"]
+    for n in (128, 256, 512, 1024):
+        p = media.linear_kappa2_problem(n)
+        for key, L, al in (("2level_alpha0.0", 2, 0.0), ("3level_alpha0.1", 3, 0.1), ("4level_alpha0.25", 4, 0.25)):
+            its = iterations(p, "rb", al, levels=L)
+            out["cells"].append({"table": "5.3-linear", "n": n, "levels": L, "alpha": al, "paper": g[key][str(n)],
+                                 "gpu": its})
+            print(json.dumps(out["cells"][-1]), flush=True)
+    g = gold["table_5_4_full"]
+    for n in (48, 64, 96, 128):
+        p = media.homogeneous_problem(3, n, sponge=20, gamma_max_over_omega=1.0)
+        for sm in ("jacobi", "element", "plus"):
+            its = iterations(p, sm, g["alpha"][sm])
+            out["cells"].append({"table": "5.4", "n": n, "smoother": sm, "paper": g[sm][str(n)], "gpu": its})
+            print(json.dumps(out["cells"][-1]), flush=True)
+    out["seconds"] = round(time.time() - t0, 1)
+    json.dump(out, open(a.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

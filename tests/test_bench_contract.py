@@ -25,3 +25,17 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+
+
+def test_gpus_2_launches_two_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under torch.distributed.run with
+    two processes (one per GPU) on a 127.0.0.1 rendezvous; --dry-run stops after a gloo
+    all-reduce that every rank joins (no CUDA)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                               "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    recs = [json.loads(l) for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert sorted(r["rank"] for r in recs) == [0, 1]
+    assert all(r["world_size"] == 2 and r["ranks_seen"] == 2 for r in recs)

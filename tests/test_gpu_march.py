@@ -1,0 +1,62 @@
+"""The 2D c64 warp-marching fine operator (k_fine_op2d_march) against the
+node-parallel kernels it replaces (HMG_NO_FMARCH=1 at build): the same per-node grouping of
+the stencil sums, so the outputs must be BIT-identical -- on ragged grids (strip width 60,
+segment height 32: sizes that leave partial strips and segments), homogeneous (uniform box)
+and heterogeneous media, through H x, H_s x, the residual, the V-cycle and FGMRES (the
+FGMRES matvec uses the fp64-sigma instance).  Parity against the oracle: test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+from helpers import DAMPING, problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+@pytest.mark.parametrize("medium,cells,stencil", [
+    ("homogeneous", (128, 128), "compact4"),
+    ("hetero", (120, 68), "compact4"),
+    ("hetero", (8, 40), "compact4"),
+    ("hetero", (64, 32), "fd2"),
+])
+def test_march_bit_identical(monkeypatch, medium, cells, stencil):
+    import torch
+    from paper_2511_16808_b200 import hmg, media
+    if medium == "homogeneous":
+        p = media.config_problem(0)
+    else:
+        p = problem(2, cells)
+    L = 3
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=L, smoother="rb", fine_stencil=stencil,
+                       damping=DAMPING[(2, "rb")], dtype="c64")
+    monkeypatch.delenv("HMG_NO_FMARCH", raising=False)
+    ga = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.3)
+    monkeypatch.setenv("HMG_NO_FMARCH", "1")
+    gb = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.3)
+    monkeypatch.delenv("HMG_NO_FMARCH")
+    x = torch.from_numpy(media.random_complex(p.n, 1)).to(torch.complex64).cuda()
+    f = torch.from_numpy(media.random_complex(p.n, 2)).to(torch.complex64).cuda()
+    for shifted in (False, True):
+        ya, yb = torch.empty_like(x), torch.empty_like(x)
+        ga.apply_helmholtz(x, ya, shifted=shifted)
+        gb.apply_helmholtz(x, yb, shifted=shifted)
+        assert torch.equal(ya, yb)
+        ga.residual(f, x, ya, shifted=shifted)
+        gb.residual(f, x, yb, shifted=shifted)
+        assert torch.equal(ya, yb)
+    q = torch.from_numpy(p.q.ravel()).to(torch.complex64).cuda()
+    za, zb = torch.zeros_like(q), torch.zeros_like(q)
+    ga.vcycle(q, za)
+    gb.vcycle(q, zb)
+    assert torch.equal(za, zb)
+    xa, xb = torch.zeros_like(q), torch.zeros_like(q)
+    ra = ga.fgmres_solve(q, xa, restart=10, tol=1e-6, maxiter=300)
+    rb = gb.fgmres_solve(q, xb, restart=10, tol=1e-6, maxiter=300)
+    assert ra.iterations == rb.iterations and ra.history == rb.history
+    assert torch.equal(xa, xb)
