@@ -159,6 +159,15 @@ HMG_API void hmg_comm_destroy(hmg_comm *comm);
 HMG_API hmg_status hmg_build_hierarchy_dist(const hmg_options *opts, const double *kappa, double omega,
                                             const double *gamma, double shift_alpha, hmg_comm *comm,
                                             void *stream, hmg_hierarchy **out);
+/* Host-only memory plan of the partitioned build for `rank` of
+ * `nranks`: per level ([levels] arrays) the setup window [wlo, whi) of slab-axis
+ * rows on which the rank computes the level's setup arrays, and the rows it keeps
+ * [klo, khi) (whole level when replicated); bytes[0] = modelled peak device bytes of
+ * the build, bytes[1] = resident bytes after it, bytes[2] = the FGMRES(20) workspace
+ * allocated by the first solve (same model as the build's allocations).  Returns the
+ * number of partitioned levels, or -1 on bad arguments.  No device is touched. */
+HMG_API int hmg_setup_plan(const hmg_options *opts, int nranks, int rank, int64_t *wlo, int64_t *whi,
+                           int64_t *klo, int64_t *khi, double *bytes);
 /* Global rows [lo, hi) of the slab axis this rank holds on `level` (0..N on
  * replicated levels and on one GPU).  Returns 0, or -1 on bad arguments. */
 HMG_API int hmg_level_rows(const hmg_hierarchy *hier, int level, int64_t *lo, int64_t *hi);

@@ -206,6 +206,23 @@ struct NcclComm : Comm {
     }
     NC(a->GroupEnd());
   }
+  void halo_multi(const std::vector<HaloReq> &rq, cudaStream_t s) override {
+    auto *a = nccl::api();
+    NC(a->GroupStart());
+    for (const HaloReq &q : rq) {
+      if (rank > 0) {
+        NC(a->Send(q.send_lo, q.bytes, nccl::Uint8, rank - 1, c, s));
+        NC(a->Recv(q.recv_lo, q.bytes, nccl::Uint8, rank - 1, c, s));
+      }
+      if (rank < size - 1) {
+        NC(a->Send(q.send_hi, q.bytes, nccl::Uint8, rank + 1, c, s));
+        NC(a->Recv(q.recv_hi, q.bytes, nccl::Uint8, rank + 1, c, s));
+      }
+    }
+    NC(a->GroupEnd());
+  }
+  // NCCL point-to-point and collectives are stream-ordered and graph-capturable
+  bool capturable() const override { return true; }
   void allreduce_sum(double *d, int n, cudaStream_t s) override {
     NC(nccl::api()->AllReduce(d, d, n, nccl::Float64, nccl::Sum, c, s));
   }

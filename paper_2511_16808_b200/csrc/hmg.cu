@@ -9,6 +9,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <complex>
@@ -263,6 +264,44 @@ static void slab_partition(const std::vector<int64_t> &Nl, int nranks, int G, st
   }
 }
 
+// Setup windows of the partitioned build: for every slab-partitioned
+// level l the global slab-axis rows [wlo, whi) on which this rank computes the
+// level's fp64 setup arrays.  They must cover (coarse to fine):
+//   - the rows the rank keeps, [lo - G, hi + G), and the patch support around them
+//     (2 rows: patch inverses of the anchors within 1 row, each reading its patch's
+//     nodes within 1 more; the RB closed form on level 0 reads sigma 1 row away);
+//   - the fine rows the next level's Galerkin product R A P (rows 2I -+ rR) -- or the
+//     REDISCRETIZE full-weighting average (2I -+ 1) -- reads for that level's window,
+//     and for the first replicated level for the rank's own share of its rows
+//     (computed here, then allgathered).
+// Replicated levels use the whole grid.  Every value a rank keeps is computed from the
+// same inputs by the same arithmetic as in the replicated build (bit-identical).
+static void plan_windows(const std::vector<int64_t> &Nl, const std::vector<int64_t> &lo,
+                         const std::vector<int64_t> &hi, const std::vector<int> &dist, int nranks, int me, int G,
+                         const std::vector<int> &rR, bool rediscretize, bool rb_fine, std::vector<int64_t> &wlo,
+                         std::vector<int64_t> &whi) {
+  const int L = (int)Nl.size();
+  wlo.assign(L, 0);
+  whi = Nl;
+  for (int l = L - 1; l >= 0; --l) {
+    if (!dist[l]) continue;
+    const int64_t plo = lo[(size_t)l * nranks + me], phi = hi[(size_t)l * nranks + me];
+    const int reach = (l == 0 && rb_fine) ? 1 : 2;
+    int64_t a = plo - G - reach, b = phi + G + reach;
+    if (l + 1 < L) {
+      const int64_t na = dist[l + 1] ? wlo[l + 1] : lo[(size_t)(l + 1) * nranks + me];
+      const int64_t nb = dist[l + 1] ? whi[l + 1] : hi[(size_t)(l + 1) * nranks + me];
+      const int rr = rediscretize ? 1 : rR[l];
+      if (nb > na) {
+        a = std::min(a, 2 * na - rr);
+        b = std::max(b, 2 * (nb - 1) + rr + 1);
+      }
+    }
+    wlo[l] = std::max<int64_t>(0, a);
+    whi[l] = std::min<int64_t>(Nl[l], b);
+  }
+}
+
 constexpr double kReorthEta2 = 0.01;  // ||w'||^2 < eta^2 ||w||^2 triggers a second CGS pass
 
 template <typename T> struct Solver : SolverBase {
@@ -288,6 +327,10 @@ template <typename T> struct Solver : SolverBase {
   };
   std::vector<Level> lev;
   int G = 2;
+  // slab partition [level * nranks + rank] and the setup windows (partitioned build)
+  std::vector<int64_t> plo, phi, wlo, whi;
+  std::vector<int> pdist;
+  bool part_setup = false;
   double omega = 0, alpha = 0;
   DBuf sig, w2k2, gq;     // fine-level coefficients
   DBuf sigd;              // fine-level sigma in fp64 (restart residual of FGMRES)
@@ -359,15 +402,39 @@ template <typename T> struct Solver : SolverBase {
       for (int a = 0; a < dim; ++a) nodes[a] = (nodes[a] - 1) / 2 + 1;
       h *= 2;
     }
-    const Geo &f0 = lev[0].geo;
-    const int64_t N0 = f0.nodes();
-    // a1: coefficients
+    for (int l = 0; l + 1 < L; ++l) level_scheme(opt.intergrid, l, lev[l].rR, lev[l].rP);
+    rb_closed = (dim == 2 && opt.smoother == HMG_VANKA_RB);
+    // slab partition and setup windows: with a communicator every rank computes the
+    // partitioned levels only on its window of rows (HMG_REPLICATED_SETUP=1: the whole
+    // grid, then sliced -- the round-1 build, kept for comparison)
+    const int ax = slab_axis();
+    const int64_t N0 = lev[0].geo.nodes();   // global fine nodes
     {
+      std::vector<int64_t> Nl(L);
+      std::vector<int> rR(L, 1);
+      for (int l = 0; l < L; ++l) Nl[l] = lev[l].geo.N[ax];
+      for (int l = 0; l + 1 < L; ++l) rR[l] = lev[l].rR;
+      wlo.assign(L, 0);
+      whi = Nl;
+      if (comm && comm->size > 1) {
+        slab_partition(Nl, comm->size, G, plo, phi, pdist);
+        part_setup = std::getenv("HMG_REPLICATED_SETUP") == nullptr;
+        if (part_setup)
+          plan_windows(Nl, plo, phi, pdist, comm->size, comm->rank, G, rR, opt.coarse_op == HMG_REDISCRETIZE,
+                       rb_closed, wlo, whi);
+      }
+      for (int l = 0; l < L; ++l) lev[l].geo = rows_geo(lev[l].geo, wlo[l], whi[l]);
+    }
+    const Geo &f0 = lev[0].geo;
+    const int64_t Nw = f0.nodes();           // nodes of the level-0 window
+    // a1: coefficients (the window's rows of the host arrays)
+    {
+      const int64_t row_nodes = dim == 3 ? (int64_t)f0.n[0] * f0.n[1] : f0.n[0];
       DBuf dk, dg;
-      dk.alloc(N0 * sizeof(double), s);
-      dg.alloc(N0 * sizeof(double), s);
-      CK(cudaMemcpyAsync(dk.p, kappa, N0 * sizeof(double), cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(dg.p, gamma, N0 * sizeof(double), cudaMemcpyHostToDevice, s));
+      dk.alloc(Nw * sizeof(double), s);
+      dg.alloc(Nw * sizeof(double), s);
+      CK(cudaMemcpyAsync(dk.p, kappa + wlo[0] * row_nodes, Nw * sizeof(double), cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dg.p, gamma + wlo[0] * row_nodes, Nw * sizeof(double), cudaMemcpyHostToDevice, s));
       w2k2.alloc(f0.total * sizeof(double), s);
       gq.alloc(f0.total * sizeof(double), s);
       sig.alloc(f0.total * sizeof(C), s);
@@ -398,7 +465,12 @@ template <typename T> struct Solver : SolverBase {
     const double *pw = w2k2.template as<double>(), *pg = gq.template as<double>();
     for (int l = 0; l + 1 < L; ++l) {
       Level &F = lev[l], &Cc = lev[l + 1];
-      level_scheme(opt.intergrid, l, F.rR, F.rP);
+      // the first replicated level of a partitioned build: this rank computes its share
+      // of the rows (cview), then every plane is allgathered
+      const bool share = part_setup && pdist[l] && !pdist[l + 1];
+      const Geo cview = share ? rows_view(Cc.geo, plo[(size_t)(l + 1) * comm->size + comm->rank],
+                                          phi[(size_t)(l + 1) * comm->size + comm->rank])
+                              : Cc.geo;
       if (opt.coarse_op == HMG_GALERKIN) {
         const int rc = (F.rR + F.r + F.rP) / 2;
         if (rc > G) throw HmgError(HMG_EINVAL, "coarse stencil radius exceeds ghost width");
@@ -407,22 +479,28 @@ template <typename T> struct Solver : SolverBase {
         const int K = kcount(dim, rc);
         cd[l + 1].alloc((size_t)K * Cc.geo.total * sizeof(double2), s);
         TransferW tw = transfer_weights(F.rR, F.rP);
-        auto nl = node_launch(Cc.geo);
+        auto nl = node_launch(cview);
+        const Geo &cg2 = cview;
         if (dim == 2) {
-          if (rc == 1) launch(k_galerkin<2, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
-          else if (rc == 2) launch(k_galerkin<2, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
-          else launch(k_galerkin<2, 3>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+          if (rc == 1) launch(k_galerkin<2, 1>, nl.grid, nl.block, 0, s, F.geo, cg2, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+          else if (rc == 2) launch(k_galerkin<2, 2>, nl.grid, nl.block, 0, s, F.geo, cg2, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+          else launch(k_galerkin<2, 3>, nl.grid, nl.block, 0, s, F.geo, cg2, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
         } else {
-          if (rc == 1) launch(k_galerkin<3, 1>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
-          else launch(k_galerkin<3, 2>, nl.grid, nl.block, 0, s, F.geo, Cc.geo, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+          if (rc == 1) launch(k_galerkin<3, 1>, nl.grid, nl.block, 0, s, F.geo, cg2, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
+          else launch(k_galerkin<3, 2>, nl.grid, nl.block, 0, s, F.geo, cg2, cd[l].template as<double2>(), F.r, tw, cd[l + 1].template as<double2>());
         }
+        if (share) gather_rows(l + 1, cd[l + 1], K, sizeof(double2), s);
       } else {
         DBuf nw, ng;
         nw.alloc(Cc.geo.total * sizeof(double), s);
         ng.alloc(Cc.geo.total * sizeof(double), s);
-        auto nl = node_launch(Cc.geo);
-        launch(k_fw_average, nl.grid, nl.block, 0, s, F.geo, Cc.geo, pw, nw.template as<double>());
-        launch(k_fw_average, nl.grid, nl.block, 0, s, F.geo, Cc.geo, pg, ng.template as<double>());
+        auto nl = node_launch(cview);
+        launch(k_fw_average, nl.grid, nl.block, 0, s, F.geo, cview, pw, nw.template as<double>());
+        launch(k_fw_average, nl.grid, nl.block, 0, s, F.geo, cview, pg, ng.template as<double>());
+        if (share) {
+          gather_rows(l + 1, nw, 1, sizeof(double), s);
+          gather_rows(l + 1, ng, 1, sizeof(double), s);
+        }
         CK(cudaStreamSynchronize(s));
         cw = std::move(nw);
         cg = std::move(ng);
@@ -440,8 +518,7 @@ template <typename T> struct Solver : SolverBase {
       Lv.coef.alloc(n * sizeof(C), s);
       launch(k_cast<T>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, cd[l].template as<double2>(), Lv.coef.template as<C>(), n);
     }
-    // Vanka patch factors
-    rb_closed = (dim == 2 && opt.smoother == HMG_VANKA_RB);
+    // Vanka patch factors (on a partitioned level only for the rows the rank keeps)
     DBuf errb;
     errb.alloc(sizeof(unsigned long long), s);
     for (int l = 0; l + 1 < L; ++l) {
@@ -456,19 +533,21 @@ template <typename T> struct Solver : SolverBase {
         const double Mc = c4 ? FineW<2, ST_COMPACT4>::Mc : FineW<2, ST_FD2>::Mc;
         const double Le = c4 ? FineW<2, ST_COMPACT4>::Le : FineW<2, ST_FD2>::Le;
         const double ih2 = 1.0 / (Lv.h * Lv.h);
-        launch(k_rb_factors<T>, nl.grid, nl.block, 0, s, Lv.geo, (const double2 *)sigd.template as<double2>(), alpha,
+        const Geo kv = keep_view(l);
+        nl = node_launch(kv);
+        launch(k_rb_factors<T>, nl.grid, nl.block, 0, s, kv, (const double2 *)sigd.template as<double2>(), alpha,
                ih2, Lc, Mc, Le * ih2, rb_ia.template as<C>(), rb_id.template as<C>());
         continue;
       }
       DBuf hv;   // fp64 patch inverses (setup scratch)
       hv.alloc((size_t)k * k * Lv.geo.total * sizeof(double2), s);
       CK(cudaMemsetAsync(errb.p, 0xff, sizeof(unsigned long long), s));
-      patch_inverse(Lv, cd[l], hv.template as<double2>(), errb.template as<unsigned long long>(), s);
+      patch_inverse(keep_view(l, 1), cd[l], Lv.r, hv.template as<double2>(), errb.template as<unsigned long long>(), s);
       unsigned long long bad = 0;
       CK(cudaMemcpyAsync(&bad, errb.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (bad != ~0ull) {
-        const int64_t nx = Lv.geo.n[0], ny = Lv.geo.n[1];
+        const int64_t nx = Lv.geo.N[0], ny = Lv.geo.N[1];   // the kernel reports GLOBAL indices
         char buf[160];
         snprintf(buf, sizeof buf, "singular Vanka patch at level %d, anchor node (%lld, %lld, %lld)", l,
                  (long long)(bad % nx), (long long)((bad / nx) % ny), (long long)(bad / (nx * ny)));
@@ -477,7 +556,7 @@ template <typename T> struct Solver : SolverBase {
       // assemble B = sum_i V_i^T W_i H_i^{-1} V_i as an NB-point stencil (fp64 sums, stored in T)
       const int nb = bstencil_planes();
       Lv.bop.alloc((size_t)nb * Lv.geo.total * sizeof(C), s);
-      assemble_vanka(Lv, hv.template as<double2>(), s);
+      assemble_vanka(keep_view(l), Lv.bop.template as<C>(), hv.template as<double2>(), s);
       CK(cudaStreamSynchronize(s));
     }
     // coarsest dense inverse (fp64)
@@ -629,6 +708,52 @@ template <typename T> struct Solver : SolverBase {
   int slab_axis() const { return opt.dim == 3 ? 2 : 1; }
   int64_t rowsize(const Geo &g) const { return opt.dim == 3 ? g.pxy : g.px; }
 
+  // the box of global slab-axis rows [a, b) of the full level box `full` (setup window)
+  Geo rows_geo(const Geo &full, int64_t a, int64_t b) const {
+    const int ax = slab_axis();
+    Geo g = full;
+    g.n[ax] = (int)(b - a);
+    g.o[ax] = (int)a;
+    g.total = rowsize(full) * (g.n[ax] + 2 * G);
+    if (opt.dim == 2) g.pxy = g.total;
+    g.slab_len = (int64_t)g.n[ax] * rowsize(full);
+    return g;
+  }
+  // global rows [a, b) of the box g addressed in g's own memory layout (kernel launch view)
+  Geo rows_view(const Geo &g, int64_t a, int64_t b) const {
+    const int ax = slab_axis();
+    Geo v = g;
+    a = std::max<int64_t>(a, g.o[ax]);
+    b = std::min<int64_t>(b, (int64_t)g.o[ax] + g.n[ax]);
+    v.n[ax] = (int)std::max<int64_t>(0, b - a);
+    v.base = g.base + (a - g.o[ax]) * rowsize(g);
+    v.o[ax] = (int)a;
+    return v;
+  }
+  // rows of level l the rank keeps (its slab +- G), widened by `extra` (patch anchors);
+  // the whole box on replicated levels / one rank
+  Geo keep_view(int l, int extra = 0) const {
+    const Geo &g = lev[l].geo;
+    if (!part_setup || !pdist[l]) return g;
+    const int P = comm->size, me = comm->rank;
+    return rows_view(g, plo[(size_t)l * P + me] - G - extra, phi[(size_t)l * P + me] + G + extra);
+  }
+  // allgather `planes` planes of a per-node array of the (replicated) level l: rank q
+  // contributes its partition rows [plo_q, phi_q) of every plane
+  void gather_rows(int l, DBuf &b, int planes, size_t esize, cudaStream_t s) {
+    const Geo &g = lev[l].geo;
+    const int P = comm->size;
+    std::vector<size_t> off(P), len(P);
+    for (int k = 0; k < planes; ++k) {
+      for (int q = 0; q < P; ++q) {
+        off[q] = ((size_t)k * g.total + (size_t)(G + plo[(size_t)l * P + q]) * rowsize(g)) * esize;
+        len[q] = (size_t)(phi[(size_t)l * P + q] - plo[(size_t)l * P + q]) * rowsize(g) * esize;
+      }
+      comm->allgatherv(b.p, off, len, s);
+    }
+    CK(cudaStreamSynchronize(s));
+  }
+
   // keep only this rank's slab (+ G ghost rows) of a per-node array of the
   // replicated setup: rows [lo - G, hi + G) are contiguous in the padded box
   void slice(DBuf &b, size_t esize, const Geo &gG, const Geo &gL, int64_t lo, cudaStream_t s) {
@@ -645,10 +770,10 @@ template <typename T> struct Solver : SolverBase {
 
   void distribute(cudaStream_t s) {
     const int ax = slab_axis(), P = comm->size, me = comm->rank;
-    std::vector<int64_t> Nl(L), lo, hi;
-    std::vector<int> dist;
+    std::vector<int64_t> Nl(L);
+    const std::vector<int64_t> &lo = plo, &hi = phi;
+    const std::vector<int> &dist = pdist;
     for (int l = 0; l < L; ++l) Nl[l] = lev[l].geo.N[ax];
-    slab_partition(Nl, P, G, lo, hi, dist);
     for (int l = 0; l < L; ++l) {
       Level &Lv = lev[l];
       Lv.lo = 0;
@@ -673,21 +798,18 @@ template <typename T> struct Solver : SolverBase {
       Lv.dist = true;
       Lv.lo = lo[(size_t)l * P + me];
       Lv.hi = hi[(size_t)l * P + me];
-      const Geo gG = Lv.geo;
-      Geo gL = gG;
-      gL.n[ax] = (int)(Lv.hi - Lv.lo);
-      gL.o[ax] = (int)Lv.lo;
-      gL.total = rowsize(gG) * (gL.n[ax] + 2 * G);
-      gL.slab_len = (int64_t)gL.n[ax] * rowsize(gG);
-      slice(Lv.coef, sizeof(C), gG, gL, Lv.lo, s);
-      slice(Lv.bop, sizeof(C), gG, gL, Lv.lo, s);
+      const Geo gG = Lv.geo;   // the setup window (the whole level in a replicated build)
+      const Geo gL = rows_geo(gG, Lv.lo, Lv.hi);
+      const int64_t r0 = Lv.lo - gG.o[ax];   // padded row of global row lo - G in the window
+      slice(Lv.coef, sizeof(C), gG, gL, r0, s);
+      slice(Lv.bop, sizeof(C), gG, gL, r0, s);
       if (l == 0) {
-        slice(sig, sizeof(C), gG, gL, Lv.lo, s);
-        slice(sigd, sizeof(D), gG, gL, Lv.lo, s);
-        slice(rb_ia, sizeof(C), gG, gL, Lv.lo, s);
-        slice(rb_id, sizeof(C), gG, gL, Lv.lo, s);
-        slice(w2k2, sizeof(double), gG, gL, Lv.lo, s);
-        slice(gq, sizeof(double), gG, gL, Lv.lo, s);
+        slice(sig, sizeof(C), gG, gL, r0, s);
+        slice(sigd, sizeof(D), gG, gL, r0, s);
+        slice(rb_ia, sizeof(C), gG, gL, r0, s);
+        slice(rb_id, sizeof(C), gG, gL, r0, s);
+        slice(w2k2, sizeof(double), gG, gL, r0, s);
+        slice(gq, sizeof(double), gG, gL, r0, s);
       }
       Lv.geo = gL;
     }
@@ -696,17 +818,28 @@ template <typename T> struct Solver : SolverBase {
   // fill `depth` slab-axis ghost rows of `nplanes` planes of a level vector
   // from the neighbouring ranks (no-op on replicated levels / one GPU)
   void halo(int l, const void *vec, int depth, cudaStream_t s, int nplanes = 1, size_t esize = 0) {
+    halos(l, {{vec, depth}}, s, nplanes, esize);
+  }
+  // the halos of several vectors of level l exchanged as ONE communication step
+  void halos(int l, std::initializer_list<std::pair<const void *, int>> vd, cudaStream_t s, int nplanes = 1,
+             size_t esize = 0) {
     const Level &Lv = lev[l];
-    if (!Lv.dist || !vec || depth <= 0) return;
+    if (!Lv.dist) return;
     if (!esize) esize = vsize(l);
     const Geo &g = Lv.geo;
     const int n = g.n[slab_axis()];
     const size_t row = (size_t)rowsize(g) * esize;
-    for (int k = 0; k < nplanes; ++k) {
-      char *b = (char *)vec + (size_t)k * g.total * esize;
-      comm->halo(b + (size_t)G * row, b + (size_t)(G - depth) * row, b + (size_t)(G + n - depth) * row,
-                 b + (size_t)(G + n) * row, (size_t)depth * row, s);
+    std::vector<Comm::HaloReq> rq;
+    for (const auto &v : vd) {
+      if (!v.first || v.second <= 0) continue;
+      const int depth = v.second;
+      for (int k = 0; k < nplanes; ++k) {
+        char *b = (char *)v.first + (size_t)k * g.total * esize;
+        rq.push_back({b + (size_t)G * row, b + (size_t)(G - depth) * row, b + (size_t)(G + n - depth) * row,
+                      b + (size_t)(G + n) * row, (size_t)depth * row});
+      }
     }
+    if (!rq.empty()) comm->halo_multi(rq, s);
   }
   void allreduce(double2 *d, int n, cudaStream_t s) {
     if (comm && comm->size > 1) comm->allreduce_sum(reinterpret_cast<double *>(d), 2 * n, s);
@@ -757,32 +890,33 @@ template <typename T> struct Solver : SolverBase {
     }
     throw HmgError(HMG_EINVAL, "unknown smoother");
   }
-  void assemble_vanka(Level &Lv, const double2 *hv, cudaStream_t s) {
-    auto nl = node_launch(Lv.geo);
-    C *B = Lv.bop.template as<C>();
+  // g: the level's window box or a view of some of its rows (same memory layout)
+  void assemble_vanka(const Geo &g, C *B, const double2 *hv, cudaStream_t s) {
+    auto nl = node_launch(g);
     const int dim = opt.dim;
     switch (opt.smoother) {
-      case HMG_VANKA_RB: launch(k_vanka_assemble<T, 2, PK_RB>, nl.grid, nl.block, 0, s, Lv.geo, hv, B); break;
+      case HMG_VANKA_RB: launch(k_vanka_assemble<T, 2, PK_RB>, nl.grid, nl.block, 0, s, g, hv, B); break;
       case HMG_VANKA_ELEMENT:
-        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
-        else launch(k_vanka_assemble<T, 3, PK_ELEMENT>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_ELEMENT>, nl.grid, nl.block, 0, s, g, hv, B);
+        else launch(k_vanka_assemble<T, 3, PK_ELEMENT>, nl.grid, nl.block, 0, s, g, hv, B);
         break;
       case HMG_JACOBI:
-        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
-        else launch(k_vanka_assemble<T, 3, PK_JACOBI>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_JACOBI>, nl.grid, nl.block, 0, s, g, hv, B);
+        else launch(k_vanka_assemble<T, 3, PK_JACOBI>, nl.grid, nl.block, 0, s, g, hv, B);
         break;
       case HMG_VANKA_PLUS:
-        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
-        else launch(k_vanka_assemble<T, 3, PK_PLUS>, nl.grid, nl.block, 0, s, Lv.geo, hv, B);
+        if (dim == 2) launch(k_vanka_assemble<T, 2, PK_PLUS>, nl.grid, nl.block, 0, s, g, hv, B);
+        else launch(k_vanka_assemble<T, 3, PK_PLUS>, nl.grid, nl.block, 0, s, g, hv, B);
         break;
     }
   }
 
   // fp64 patch inverses H_i^{-1} into hv [K*K][total] (setup scratch)
-  void patch_inverse(Level &Lv, DBuf &cd, double2 *hv, unsigned long long *err, cudaStream_t s) {
-    auto nl = node_launch(Lv.geo);
+  void patch_inverse(const Geo &g, DBuf &cd, int r, double2 *hv, unsigned long long *err, cudaStream_t s) {
+    auto nl = node_launch(g);
     const double2 *c = cd.template as<double2>();
     const int dim = opt.dim;
+    struct { const Geo &geo; int r; } Lv{g, r};
     switch (opt.smoother) {
       case HMG_VANKA_RB:
         if (dim != 2) throw HmgError(HMG_EINVAL, "RB patch is 2D only (the paper rejects the 13-node 3D RB patch, P:949-951)");
@@ -1130,8 +1264,7 @@ template <typename T> struct Solver : SolverBase {
       const C *ia = rb_ia.template as<C>(), *id = rb_id.template as<C>();
       const C *ff = (const C *)f, *ui = (const C *)u;
       C *uo = (C *)u_out;
-      if (!zero) halo(0, u, 3, s);
-      halo(0, f, 2, s);
+      halos(0, {{zero ? nullptr : u, 3}, {f, 2}}, s);   // one exchange for both
       // algorithmic bytes: f, u' (+ u) per node; ia, id (+ sigma) outside the uniform box
       tag(zero ? "smooth_rb2d_fine_zero" : "smooth_rb2d_fine", 0,
           (zero ? 2 : 3) * sizeof(C) * nn + (zero ? 2 : 3) * sizeof(C) * outside(0));
@@ -1209,7 +1342,12 @@ template <typename T> struct Solver : SolverBase {
     });
   }
 
-  bool graphs_ok() const { return (!comm || comm->size == 1) && !prof_active() && std::getenv("HMG_NO_GRAPHS") == nullptr; }
+  // CUDA graphs: on one GPU, and with a communicator whose calls are stream-ordered
+  // device work (NCCL: its halos and the coarse allgather are captured with the cycle)
+  bool graphs_ok() const {
+    return (!comm || comm->size == 1 || comm->capturable()) && !prof_active() &&
+           std::getenv("HMG_NO_GRAPHS") == nullptr;
+  }
 
   // levels >= 1 of the cycle (zero initial guess on lev[1].u, rhs lev[1].f)
   // as one CUDA graph launch, on a private stream ordered against the caller's
@@ -1987,6 +2125,75 @@ int hmg_slab_partition(int64_t nodes0, int levels, int nranks, int ghost, int64_
   int nd = 0;
   for (int l = 0; l < levels; ++l) { dist[l] = d2[l]; nd += d2[l]; }
   return nd;
+}
+
+int hmg_setup_plan(const hmg_options *o, int nranks, int rank, int64_t *wlo, int64_t *whi, int64_t *klo,
+                   int64_t *khi, double *bytes) {
+  try {
+    if (!o || nranks < 1 || rank < 0 || rank >= nranks || !wlo || !whi || !klo || !khi || !bytes) return -1;
+    if ((o->dim != 2 && o->dim != 3) || o->levels < 2 || o->levels > 16) return -1;
+    const int dim = o->dim, L = o->levels, ax = dim == 3 ? 2 : 1;
+    const int G = nranks > 1 ? (o->intergrid == HMG_CUBIC ? 5 : 4) : (o->intergrid == HMG_CUBIC ? 3 : 2);
+    const double s = o->dtype == HMG_C64 ? 8.0 : 16.0;
+    std::vector<std::array<int64_t, 3>> n(L);
+    for (int a = 0; a < 3; ++a) n[0][a] = a < dim ? o->cells[a] + 1 : 1;
+    for (int l = 1; l < L; ++l)
+      for (int a = 0; a < 3; ++a) n[l][a] = a < dim ? (n[l - 1][a] - 1) / 2 + 1 : 1;
+    std::vector<int64_t> Nl(L);
+    for (int l = 0; l < L; ++l) Nl[l] = n[l][ax];
+    std::vector<int> rR(L, 1), rP(L, 1), r(L, 1);
+    for (int l = 0; l + 1 < L; ++l) hmg::level_scheme(o->intergrid, l, rR[l], rP[l]);
+    for (int l = 0; l + 1 < L; ++l) r[l + 1] = o->coarse_op == HMG_GALERKIN ? (rR[l] + r[l] + rP[l]) / 2 : 1;
+    std::vector<int64_t> lo, hi, wl, wh;
+    std::vector<int> dist;
+    hmg::slab_partition(Nl, nranks, G, lo, hi, dist);
+    const bool rb = dim == 2 && o->smoother == HMG_VANKA_RB;
+    hmg::plan_windows(Nl, lo, hi, dist, nranks, rank, G, rR, o->coarse_op == HMG_REDISCRETIZE, rb, wl, wh);
+    auto kc = [&](int rr) { return dim == 3 ? (2 * rr + 1) * (2 * rr + 1) * (2 * rr + 1) : (2 * rr + 1) * (2 * rr + 1); };
+    const int pk = o->smoother == HMG_JACOBI ? 1 : o->smoother == HMG_VANKA_ELEMENT ? (1 << dim)
+                   : o->smoother == HMG_VANKA_PLUS ? 2 * dim + 1 : 5;
+    const int nb = o->smoother == HMG_JACOBI ? 1 : o->smoother == HMG_VANKA_ELEMENT ? (dim == 3 ? 27 : 9)
+                   : (o->smoother == HMG_VANKA_PLUS && dim == 3) ? 25 : 13;
+    auto padded = [&](int l, int64_t rows) {   // padded box elements of `rows` slab-axis rows
+      const int64_t px = (n[l][0] + 2 * G + 7) / 8 * 8;
+      const int64_t rs = dim == 3 ? px * (n[l][1] + 2 * G) : px;
+      return (double)rs * (double)(rows + 2 * G);
+    };
+    double peak = 0, resident = 0, hvmax = 0;
+    int nd = 0;
+    for (int l = 0; l < L; ++l) {
+      nd += dist[l];
+      wlo[l] = wl[l];
+      whi[l] = wh[l];
+      klo[l] = dist[l] ? lo[(size_t)l * nranks + rank] : 0;
+      khi[l] = dist[l] ? hi[(size_t)l * nranks + rank] : Nl[l];
+      const double W = padded(l, wh[l] - wl[l]), Kp = padded(l, khi[l] - klo[l]);
+      const int K = kc(r[l]);
+      peak += 16.0 * K * W;                                  // fp64 stencil (setup)
+      if (l > 0) { peak += s * K * W; resident += s * K * Kp; }   // stored stencil
+      if (l + 1 < L) {
+        if (l == 0 && rb) { peak += 2 * s * W; resident += 2 * s * Kp; }   // RB factors
+        else { peak += s * nb * W; resident += s * nb * Kp; hvmax = std::max(hvmax, 16.0 * pk * pk * W); }
+      }
+      resident += 3.0 * (l == 0 ? s : 16.0) * Kp;            // cycle vectors u, f, r
+      if (l == 0) {
+        peak += (16.0 + s + 16.0) * W;                       // w2k2 + gq, sigma (T), sigma (fp64)
+        resident += (16.0 + s + 16.0) * Kp;
+      }
+    }
+    const double Nc = (double)n[L - 1][0] * n[L - 1][1] * n[L - 1][2];
+    peak += hvmax + 3.0 * Nc * Nc * 16.0;                   // patch-inverse scratch, dense A + inverse
+    resident += Nc * Nc * 16.0;
+    const double N0 = (double)n[0][0] * n[0][1] * n[0][2];
+    resident += N0 * s;                                      // io staging of the host entry points
+    const double K0p = padded(0, khi[0] - klo[0]);
+    bytes[0] = peak;
+    bytes[1] = resident;
+    bytes[2] = K0p * (41.0 * s + 3.0 * 16.0);                // FGMRES(20) basis V, Z + fp64 x, q, r
+    return nd;
+  } catch (...) {
+    return -1;
+  }
 }
 
 int hmg_level_rows(const hmg_hierarchy *h, int level, int64_t *lo, int64_t *hi) {

@@ -88,10 +88,20 @@ __host__ __device__ __forceinline__ int floordiv2(int a) { return a >= 0 ? a / 2
 //   A_c[I, J] = sum_{i in supp R(I)} sum_{j} R[I,i] A_f[i,j] P[j,J],
 //   R[I, 2I+k] = prod wR(k_a);  P[j, J] = 2^d prod wP(j_a - 2J_a)  (P = 2^d R_P^T).
 // Out-of-domain fine/coarse nodes are skipped (truncated R and P, reading A5).
+// Coarse and fine boxes may be windows of the global grid (partitioned setup,
+// Geo::o): all index arithmetic below is in GLOBAL coordinates, converted to the
+// local box only to address memory.
 template <int DIM, int RC>
 __global__ void k_galerkin(Geo gf, Geo gc, const double2 *__restrict__ cf, int rf, TransferW tw,
                            double2 *__restrict__ cc) {
-  HMG_NODE_IDX(gc, X, Y, Z);
+  HMG_NODE_IDX(gc, Xl, Yl, Zl);
+  const int X = Xl + gc.o[0], Y = Yl + gc.o[1], Z = Zl + gc.o[2];   // global coarse node
+  auto finside = [&](int x, int y, int z) {   // global fine node in the domain
+    return x >= 0 && x < gf.N[0] && y >= 0 && y < gf.N[1] && z >= 0 && z < gf.N[2];
+  };
+  auto cinside = [&](int x, int y, int z) {
+    return x >= 0 && x < gc.N[0] && y >= 0 && y < gc.N[1] && z >= 0 && z < gc.N[2];
+  };
   constexpr int WC = 2 * RC + 1;
   constexpr int KC = DIM == 3 ? WC * WC * WC : WC * WC;
   double2 acc[KC];
@@ -103,17 +113,17 @@ __global__ void k_galerkin(Geo gf, Geo gc, const double2 *__restrict__ cf, int r
     for (int ky = -tw.rR; ky <= tw.rR; ++ky)
       for (int kx = -tw.rR; kx <= tw.rR; ++kx) {
         const int ix = 2 * X + kx, iy = 2 * Y + ky, iz = DIM == 3 ? 2 * Z + kz : 0;
-        if (!gf.inside(ix, iy, iz)) continue;
+        if (!finside(ix, iy, iz)) continue;
         double wr = tw.wR[kx + tw.rR] * tw.wR[ky + tw.rR];
         if (DIM == 3) wr *= tw.wR[kz + tw.rR];
-        const int64_t fi = gf.idx(ix, iy, iz);
+        const int64_t fi = gf.idx(ix - gf.o[0], iy - gf.o[1], iz - gf.o[2]);
         for (int oz = -ozr; oz <= ozr; ++oz)
           for (int oy = -rf; oy <= rf; ++oy)
             for (int ox = -rf; ox <= rf; ++ox) {
               const double2 a = cf[(int64_t)kidx(ox, oy, oz, rf, DIM) * gf.total + fi];
               if (a.x == 0.0 && a.y == 0.0) continue;
               const int jx = ix + ox, jy = iy + oy, jz = iz + oz;
-              if (!gf.inside(jx, jy, jz)) continue;
+              if (!finside(jx, jy, jz)) continue;
               const int jzlo = DIM == 3 ? -floordiv2(-(jz - tw.rP)) : 0;
               const int jzhi = DIM == 3 ? floordiv2(jz + tw.rP) : 0;
               const int jylo = -floordiv2(-(jy - tw.rP)), jyhi = floordiv2(jy + tw.rP);
@@ -121,7 +131,7 @@ __global__ void k_galerkin(Geo gf, Geo gc, const double2 *__restrict__ cf, int r
               for (int Jz = jzlo; Jz <= jzhi; ++Jz)
                 for (int Jy = jylo; Jy <= jyhi; ++Jy)
                   for (int Jx = jxlo; Jx <= jxhi; ++Jx) {
-                    if (!gc.inside(Jx, Jy, Jz)) continue;
+                    if (!cinside(Jx, Jy, Jz)) continue;
                     double wp = pscale * tw.wP[jx - 2 * Jx + tw.rP] * tw.wP[jy - 2 * Jy + tw.rP];
                     if (DIM == 3) wp *= tw.wP[jz - 2 * Jz + tw.rP];
                     const int dx = Jx - X, dy = Jy - Y, dz = Jz - Z;
@@ -133,14 +143,15 @@ __global__ void k_galerkin(Geo gf, Geo gc, const double2 *__restrict__ cf, int r
                   }
             }
       }
-  const int64_t ci = gc.idx(X, Y, Z);
+  const int64_t ci = gc.idx(Xl, Yl, Zl);
   for (int k = 0; k < KC; ++k) cc[(int64_t)k * gc.total + ci] = acc[k];
 }
 
 // a7 (REDISCRETIZE): full-weighting average of a per-node field, normalised
 // by the in-domain weight sum (truncated lin R, reading A13).
 static __global__ void k_fw_average(Geo gf, Geo gc, const double *__restrict__ ff, double *__restrict__ fc) {
-  HMG_NODE_IDX(gc, X, Y, Z);
+  HMG_NODE_IDX(gc, Xl, Yl, Zl);
+  const int X = Xl + gc.o[0], Y = Yl + gc.o[1], Z = Zl + gc.o[2];   // global (windows: Geo::o)
   const double w1[3] = {0.25, 0.5, 0.25};
   const int zr = gc.dim == 3 ? 1 : 0;
   double s = 0, ws = 0;
@@ -148,12 +159,12 @@ static __global__ void k_fw_average(Geo gf, Geo gc, const double *__restrict__ f
     for (int ky = -1; ky <= 1; ++ky)
       for (int kx = -1; kx <= 1; ++kx) {
         const int ix = 2 * X + kx, iy = 2 * Y + ky, iz = gc.dim == 3 ? 2 * Z + kz : 0;
-        if (!gf.inside(ix, iy, iz)) continue;
+        if (ix < 0 || ix >= gf.N[0] || iy < 0 || iy >= gf.N[1] || iz < 0 || iz >= gf.N[2]) continue;
         double w = w1[kx + 1] * w1[ky + 1] * (gc.dim == 3 ? w1[kz + 1] : 1.0);
-        s += w * ff[gf.idx(ix, iy, iz)];
+        s += w * ff[gf.idx(ix - gf.o[0], iy - gf.o[1], iz - gf.o[2])];
         ws += w;
       }
-  fc[gc.idx(X, Y, Z)] = s / ws;
+  fc[gc.idx(Xl, Yl, Zl)] = s / ws;
 }
 
 // cast a stored stencil (double) to the working precision
@@ -241,8 +252,9 @@ __global__ void k_patch_inverse(Geo g, const double2 *__restrict__ coef, int r, 
       A[a][b] = v;
     }
   const bool ok = small_inverse<K>(A, X, m);
-  if (!ok) {
-    const unsigned long long lin = (unsigned long long)(((int64_t)iz * g.n[1] + iy) * g.n[0] + ix);
+  if (!ok) {   // GLOBAL linear index of the anchor (windows / views: Geo::o)
+    const unsigned long long lin =
+        (unsigned long long)(((int64_t)(iz + g.o[2]) * g.N[1] + iy + g.o[1]) * g.N[0] + ix + g.o[0]);
     atomicMin(err, lin);
   }
   for (int a = 0; a < K; ++a)

@@ -64,6 +64,19 @@ struct Comm {
   // the matching blocks into recv_lo (from rank-1) and recv_hi (from rank+1)
   virtual void halo(const void *send_lo, void *recv_lo, const void *send_hi, void *recv_hi, size_t bytes,
                     cudaStream_t s) = 0;
+  // several halo exchanges as ONE communication step (NCCL: one group; LOCAL: in turn)
+  struct HaloReq {
+    const void *send_lo;
+    void *recv_lo;
+    const void *send_hi;
+    void *recv_hi;
+    size_t bytes;
+  };
+  virtual void halo_multi(const std::vector<HaloReq> &rq, cudaStream_t s) {
+    for (const HaloReq &r : rq) halo(r.send_lo, r.recv_lo, r.send_hi, r.recv_hi, r.bytes, s);
+  }
+  // may the calls be captured into a CUDA graph (stream-ordered device work only)?
+  virtual bool capturable() const { return false; }
   virtual void allreduce_sum(double *d, int n, cudaStream_t s) = 0;   // in place, device fp64
   // rank q owns bytes [off[q], off[q] + len[q]) of buf (same layout on every
   // rank); afterwards every rank holds all of them

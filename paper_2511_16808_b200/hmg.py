@@ -86,6 +86,8 @@ _sigs = {
     "hmg_comm_destroy": ([_vp], None),
     "hmg_build_hierarchy_dist": ([ctypes.POINTER(_Options), _vp, _d, _vp, _d, _vp, _vp, ctypes.POINTER(_vp)], _i),
     "hmg_level_rows": ([_vp, _i, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i),
+    "hmg_setup_plan": ([ctypes.POINTER(_Options), _i, _i, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                        ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_d)], _i),
     "hmg_slab_partition": ([_i64, _i, _i, _i, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i)], _i),
     "hmg_last_error": ([], ctypes.c_char_p),
     "hmg_version": ([], ctypes.c_char_p),
@@ -195,6 +197,21 @@ class LocalGroup:
             self._h = None
 
 
+def setup_plan(opts, nranks, rank):
+    """Host-only memory plan of the partitioned build (hmg_setup_plan): dict with per-level
+    setup windows and kept rows, and the modelled peak / resident / FGMRES(20) bytes."""
+    o = opts.to_c()
+    L = opts.levels
+    arr = [(ctypes.c_int64 * L)() for _ in range(4)]
+    b = (ctypes.c_double * 3)()
+    nd = _lib.hmg_setup_plan(ctypes.byref(o), nranks, rank, *arr, b)
+    if nd < 0:
+        raise HmgError(EINVAL, "bad arguments")
+    wlo, whi, klo, khi = ([int(v) for v in a] for a in arr)
+    return {"partitioned_levels": nd, "window": list(zip(wlo, whi)), "kept": list(zip(klo, khi)),
+            "setup_peak_bytes": b[0], "resident_bytes": b[1], "fgmres20_bytes": b[2]}
+
+
 def slab_partition(nodes0, levels, nranks, ghost=4):
     """Host-only partition rule (hmg_slab_partition): (lo, hi) arrays [levels, nranks], dist [levels]."""
     lo = (ctypes.c_int64 * (levels * nranks))()
@@ -236,29 +253,35 @@ class Options:
     damping: list = field(default_factory=lambda: [0.83, 0.5, 0.4, 0.65])
     dtype: str = "c128"
 
+    def to_c(self):
+        """The hmg_options struct (marshalling only); keeps the damping array alive on it."""
+        o = _Options()
+        o.dim = self.dim
+        cells = list(self.cells) + [0] * (3 - len(self.cells))
+        for a in range(3):
+            o.cells[a] = int(cells[a])
+        o.h = float(self.h)
+        o.levels = int(self.levels)
+        o.nu1, o.nu2 = int(self.nu1), int(self.nu2)
+        o.cycle = {"V": 0, "W": 1}[self.cycle]
+        o.fine_stencil = _NAMES[self.fine_stencil]
+        o.intergrid = _NAMES[self.intergrid]
+        o.coarse_op = _NAMES[self.coarse_op]
+        o.smoother = _NAMES[self.smoother]
+        o._damp = (ctypes.c_double * len(self.damping))(*[float(x) for x in self.damping])
+        o.damping = ctypes.cast(o._damp, ctypes.POINTER(ctypes.c_double))
+        o.n_damping = len(self.damping)
+        o.dtype = {"c64": C64, "c128": C128}[self.dtype]
+        return o
+
 
 class Hierarchy:
     """Owns an hmg_hierarchy handle (hmg_build_hierarchy ... hmg_hierarchy_destroy)."""
 
     def __init__(self, opts: Options, kappa, omega, gamma, alpha, stream=None, comm: "Comm" = None):
         import torch
-        o = _Options()
-        o.dim = opts.dim
-        cells = list(opts.cells) + [0] * (3 - len(opts.cells))
-        for a in range(3):
-            o.cells[a] = int(cells[a])
-        o.h = float(opts.h)
-        o.levels = int(opts.levels)
-        o.nu1, o.nu2 = int(opts.nu1), int(opts.nu2)
-        o.cycle = {"V": 0, "W": 1}[opts.cycle]
-        o.fine_stencil = _NAMES[opts.fine_stencil]
-        o.intergrid = _NAMES[opts.intergrid]
-        o.coarse_op = _NAMES[opts.coarse_op]
-        o.smoother = _NAMES[opts.smoother]
-        self._damp = (ctypes.c_double * len(opts.damping))(*[float(x) for x in opts.damping])
-        o.damping = ctypes.cast(self._damp, ctypes.POINTER(ctypes.c_double))
-        o.n_damping = len(opts.damping)
-        o.dtype = {"c64": C64, "c128": C128}[opts.dtype]
+        o = opts.to_c()
+        self._o = o
         self.opts = opts
         self.dtype = torch.complex64 if opts.dtype == "c64" else torch.complex128
         k = np.ascontiguousarray(np.asarray(kappa, dtype=np.float64).ravel())

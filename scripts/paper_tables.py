@@ -31,6 +31,16 @@ def iterations(p, smoother, alpha, intergrid="levdep", levels=4, dtype="c128"):
     return rep.iterations if rep.converged else None
 
 
+def safe_iterations(*a, **k):
+    """None where the CUDA path cannot run the cell: the 2-level cycles at 512^2 / 1024^2 need a
+    direct solve of a 257^2 / 513^2 coarse grid, beyond the dense coarsest inverse (8 GB cap)."""
+    from paper_2511_16808_b200.hmg import HmgError
+    try:
+        return iterations(*a, **k)
+    except HmgError as e:
+        return "skipped: " + str(e)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_paper_tables.json"))
@@ -44,7 +54,7 @@ def main():
         p = media.homogeneous_problem(2, n, sponge=20, gamma_max_over_omega=1.0)
         for sm in ("jacobi", "element", "plus", "rb"):
             for ig in ("cubic", "mixed", "levdep"):
-                its = iterations(p, sm, g["alpha"][sm], ig)
+                its = safe_iterations(p, sm, g["alpha"][sm], ig)
                 out["cells"].append({"table": "5.2", "n": n, "smoother": sm, "intergrid": ig,
                                      "paper": g[sm][ig][str(n)], "gpu": its})
                 print(json.dumps(out["cells"][-1]), flush=True)
@@ -52,7 +62,7 @@ def main():
     for n in (128, 256, 512, 1024):
         p = media.linear_kappa2_problem(n)
         for key, L, al in (("2level_alpha0.0", 2, 0.0), ("3level_alpha0.1", 3, 0.1), ("4level_alpha0.25", 4, 0.25)):
-            its = iterations(p, "rb", al, levels=L)
+            its = safe_iterations(p, "rb", al, levels=L)
             out["cells"].append({"table": "5.3-linear", "n": n, "levels": L, "alpha": al, "paper": g[key][str(n)],
                                  "gpu": its})
             print(json.dumps(out["cells"][-1]), flush=True)
@@ -60,7 +70,7 @@ def main():
     for n in (48, 64, 96, 128):
         p = media.homogeneous_problem(3, n, sponge=20, gamma_max_over_omega=1.0)
         for sm in ("jacobi", "element", "plus"):
-            its = iterations(p, sm, g["alpha"][sm])
+            its = safe_iterations(p, sm, g["alpha"][sm])
             out["cells"].append({"table": "5.4", "n": n, "smoother": sm, "paper": g[sm][str(n)], "gpu": its})
             print(json.dumps(out["cells"][-1]), flush=True)
     out["seconds"] = round(time.time() - t0, 1)

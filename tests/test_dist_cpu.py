@@ -72,3 +72,30 @@ def test_gloo_bootstrap_world2():
     assert all(o[1] for o in out), "unique id not broadcast"
     assert all(o[2] == 2.0 for o in out), "max over ranks"
     assert out[0][3] == (0, 2048) and out[1][3] == (2048, 4097)
+
+
+def test_setup_plan_config4_fits_8_ranks():
+    """Partitioned build: BASELINE configs[4] at full size (768^2 x 384 cells,
+    7 levels, element Vanka, c64).  On one GPU the modelled build peak is far above 180 GB;
+    slab-partitioned over 8 ranks every rank's peak and its resident + FGMRES(20) bytes fit
+    in 180 GB.  The kept rows of every partitioned level tile the level exactly, and each
+    setup window holds its kept rows and G = 4 ghost rows (host-only: no device)."""
+    from paper_2511_16808_b200 import hmg
+    o = hmg.Options(dim=3, cells=(768, 768, 384), h=25.0, levels=7, smoother="element",
+                    damping=[1.1, 0.7, 0.45, 0.6], dtype="c64")
+    one = hmg.setup_plan(o, 1, 0)
+    assert one["partitioned_levels"] == 0 and one["setup_peak_bytes"] > 180e9
+    plans = [hmg.setup_plan(o, 8, r) for r in range(8)]
+    nd = plans[0]["partitioned_levels"]
+    assert nd >= 2
+    for pl in plans:
+        assert pl["setup_peak_bytes"] < 180e9
+        assert pl["resident_bytes"] + pl["fgmres20_bytes"] < 180e9
+    for l in range(nd):
+        kept = sorted(pl["kept"][l] for pl in plans)
+        assert kept[0][0] == 0 and all(a[1] == b[0] for a, b in zip(kept, kept[1:]))
+        for pl in plans:
+            (wl, wh), (kl, kh) = pl["window"][l], pl["kept"][l]
+            assert wl <= max(0, kl - 4) and wh >= kh + 4 or wh == [385, 193, 97][l]
+    # peak per rank scales down with the rank count (about 1/N of the level-0 work plus margins)
+    assert max(p["setup_peak_bytes"] for p in plans) < 0.35 * one["setup_peak_bytes"]
