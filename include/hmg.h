@@ -32,10 +32,13 @@
  *
  * Ownership: the library copies kappa/gamma at build time; vector arguments
  * are caller-owned and only read/written during the call (stream-ordered).
- * A hierarchy is immutable after build.  One hierarchy owns one
- * workspace: calls on the same hierarchy must be serialised by the caller
- * (same stream, or external synchronisation); distinct hierarchies are
- * independent.
+ * A hierarchy is immutable after build.  Workspaces are per STREAM
+ * (SURVEY §8(b)): the first stream a call runs on uses the
+ * build's workspace, every other stream gets its own on first use (level
+ * vectors, Krylov basis, graphs, staging; the coefficients are shared), so
+ * calls on different streams may run concurrently from different host
+ * threads.  Calls on one stream must be serialised by the caller.  A
+ * slab-partitioned hierarchy serves one stream (HMG_EINVAL otherwise).
  */
 #ifndef HMG_H
 #define HMG_H

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -87,19 +88,28 @@ void prof_after(cudaStream_t s, int i) {
 struct DBuf {
   void *p = nullptr;
   size_t bytes = 0;
+  bool own = true;   // false: a view of another DBuf's memory (per-stream workspaces share coefficients)
   DBuf() = default;
   DBuf(const DBuf &) = delete;
   DBuf &operator=(const DBuf &) = delete;
-  DBuf(DBuf &&o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf(DBuf &&o) noexcept : p(o.p), bytes(o.bytes), own(o.own) { o.p = nullptr; o.bytes = 0; o.own = true; }
   DBuf &operator=(DBuf &&o) noexcept {
-    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; own = o.own; o.p = nullptr; o.bytes = 0; o.own = true; }
     return *this;
   }
   ~DBuf() { release(); }
+  static DBuf view(const DBuf &o) {
+    DBuf v;
+    v.p = o.p;
+    v.bytes = o.bytes;
+    v.own = false;
+    return v;
+  }
   void release() {
-    if (p) cudaFree(p);
+    if (p && own) cudaFree(p);
     p = nullptr;
     bytes = 0;
+    own = true;
   }
   void alloc(size_t n, cudaStream_t s) {
     release();
@@ -128,14 +138,15 @@ static void level_scheme(int scheme, int l, int &rR, int &rP) {
 // cuTensorMapEncodeTiled comes from the driver through the runtime's entry-point
 // query (no libcuda link dependency).
 static CUtensorMap make_tmap(const void *base, int esz, const Geo &g, int bx, int by) {
-  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-  if (!enc) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 enc = [] {   // thread-safe one-time lookup
     cudaDriverEntryPointQueryResult q;
     void *fn = nullptr;
-    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess) throw HmgError(HMG_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!enc) throw HmgError(HMG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap m;
   const int w = esz / 8;
   const int nz = g.dim == 3 ? g.n[2] + 2 * g.G : 1;
@@ -232,6 +243,8 @@ struct SolverBase {
   virtual int copy_stencil(int level, double *out, int64_t cap) = 0;
   virtual void level_rows(int level, int64_t *lo, int64_t *hi) const = 0;
   virtual int64_t uniform_box(int level, int64_t *lo, int64_t *hi) const = 0;
+  // a solver sharing this one's (immutable) hierarchy with a workspace of its own
+  virtual std::unique_ptr<SolverBase> clone_workspace(cudaStream_t s) const = 0;
 };
 
 // Slab partition: level-0 rows of the slowest axis split
@@ -338,6 +351,7 @@ template <typename T> struct Solver : SolverBase {
   bool rb_closed = false; // fine level uses the closed-form RB patch solve
   bool stage3d = true;    // 3D fine operator: z-marching staged kernel (HMG_NO_STAGE3D=1 at build: the gather)
   bool fmarch = true;     // 2D c64 fine operator: warp-marching kernel (HMG_NO_FMARCH=1 at build: node-parallel)
+  bool rbfast = true;     // RB sweep: constant-coefficient interior warps (HMG_NO_RB_FAST=1 at build: generic)
   DBuf rb_ia, rb_id;      // its sigma-only factors 1/a_j and 1/(a_c - e^2 sum 1/a_l), stored in T
   C usig{}, uia{}, uid{};  // level-0 uniform-box values of sig, rb_ia, rb_id
   D usigd{};
@@ -390,6 +404,7 @@ template <typename T> struct Solver : SolverBase {
     G = opt.intergrid == HMG_CUBIC ? 3 : 2;
     stage3d = std::getenv("HMG_NO_STAGE3D") == nullptr;
     fmarch = std::getenv("HMG_NO_FMARCH") == nullptr;
+    rbfast = std::getenv("HMG_NO_RB_FAST") == nullptr;
     if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
     lev.resize(L);
     int64_t nodes[3] = {opt.cells[0] + 1, opt.cells[1] + 1, dim == 3 ? opt.cells[2] + 1 : 1};
@@ -1297,8 +1312,18 @@ template <typename T> struct Solver : SolverBase {
         // zero sweep: 4 blocks/SM, unrolled x2; non-zero: 3 blocks/SM, unrolled x3 (the
         // period of its rolling windows; measured 104 / 158 ms per solve at N = 4096,
         // against 116 / 169 without unrolling; x3 spills the zero sweep at 4 blocks/SM)
-        if (zero) go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2>, 3);
-        else go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3>, 5);
+        // with a uniform box: the interior warps run the constant-coefficient instance
+        // (MODE 1), the others the generic one (MODE 2); bit-identical to MODE 0
+        if (Lv.ub.empty() || !rbfast) {
+          if (zero) go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2>, 3);
+          else go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3>, 5);
+        } else if (zero) {
+          go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2, 1>, 3);
+          go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2, 2>, 3);
+        } else {
+          go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3, 1>, 5);
+          go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3, 2>, 5);
+        }
         return;
       }
       if (zero) {
@@ -1552,7 +1577,7 @@ template <typename T> struct Solver : SolverBase {
   template <typename TV, typename TW>
   void mdot(const cplx<TV> *Vb, int nv, const cplx<TW> *w, double2 *out, cudaStream_t s, bool self = false) {
     const Geo &g = g0();
-    tag("multidot", 0, (nv * sizeof(cplx<TV>) + sizeof(cplx<TW>)) * (double)g.slab_len);
+    tag("multidot", 0, (nv * sizeof(cplx<TV>) + sizeof(cplx<TW>)) * (double)g.nodes());   // algorithmic: nodes, not padded rows
     const int nb = krylov_multidot<TV, TW>(nv, self, Vb + g.slab_off, g.total, w + g.slab_off, g.slab_len,
                                            partial.template as<double2>(), s);
     tag("reduce", 0, 16.0 * (nv + self) * nb);
@@ -1564,7 +1589,7 @@ template <typename T> struct Solver : SolverBase {
   void maxpy(const cplx<TV> *Vb, int nv, const double2 *coef, double sgn, cplx<TW> *w, double2 *nrm_out,
              cudaStream_t s, const double *vscale = nullptr) {
     const Geo &g = g0();
-    tag("multi_axpy", 0, (nv * sizeof(cplx<TV>) + 2.0 * sizeof(cplx<TW>)) * (double)g.slab_len);
+    tag("multi_axpy", 0, (nv * sizeof(cplx<TV>) + 2.0 * sizeof(cplx<TW>)) * (double)g.nodes());
     const int nb = krylov_axpy<TV, TW>(nv, Vb + g.slab_off, g.total, coef, vscale, sgn, w + g.slab_off, g.slab_len,
                                        nrm_out ? partial.template as<double2>() : (double2 *)nullptr, s);
     if (nrm_out) {
@@ -1584,7 +1609,7 @@ template <typename T> struct Solver : SolverBase {
   }
   template <typename TI, typename TO> void scale(const cplx<TI> *w, cplx<TO> *v, double a, cudaStream_t s) {
     const Geo &g = g0();
-    tag("scale", 0, (sizeof(cplx<TI>) + sizeof(cplx<TO>)) * (double)g.slab_len);
+    tag("scale", 0, (sizeof(cplx<TI>) + sizeof(cplx<TO>)) * (double)g.nodes());
     launch(k_scale<TI, TO>, dim3(nblk), dim3(KRY_THREADS), 0, s, w + g.slab_off, v + g.slab_off, a, g.slab_len);
   }
   // w = H z for the Arnoldi process: T storage of z and w, fp64 sigma and fp64
@@ -1988,6 +2013,58 @@ template <typename T> struct Solver : SolverBase {
     return st_out;
   }
 
+  // ------------------------------------------------------------ per-stream workspaces
+  // A second solver over the SAME hierarchy: coefficient arrays (stencils, Vanka
+  // operators, sigma, RB factors, coarsest inverse) are shared as non-owning views of
+  // this solver's buffers; level vectors, Krylov basis, events, graphs and pinned
+  // staging are its own.  (One per stream.)
+  std::unique_ptr<SolverBase> clone_workspace(cudaStream_t s) const override {
+    std::unique_ptr<Solver<T>> c(new Solver<T>);
+    c->opt = opt;
+    c->damping = damping;
+    c->L = L;
+    c->comm = comm;
+    c->G = G;
+    c->omega = omega;
+    c->alpha = alpha;
+    c->plo = plo; c->phi = phi; c->wlo = wlo; c->whi = whi; c->pdist = pdist;
+    c->part_setup = part_setup;
+    c->rb_closed = rb_closed;
+    c->stage3d = stage3d;
+    c->fmarch = fmarch;
+    c->rbfast = rbfast;
+    c->usig = usig; c->uia = uia; c->uid = uid; c->usigd = usigd;
+    c->sig = DBuf::view(sig);
+    c->sigd = DBuf::view(sigd);
+    c->w2k2 = DBuf::view(w2k2);
+    c->gq = DBuf::view(gq);
+    c->rb_ia = DBuf::view(rb_ia);
+    c->rb_id = DBuf::view(rb_id);
+    c->ainv = DBuf::view(ainv);
+    c->lev.resize(L);
+    for (int l = 0; l < L; ++l) {
+      const Level &a = lev[l];
+      Level &b = c->lev[l];
+      b.geo = a.geo; b.h = a.h; b.r = a.r; b.rR = a.rR; b.rP = a.rP;
+      b.dist = a.dist; b.lo = a.lo; b.hi = a.hi; b.gather_in = a.gather_in; b.view = a.view;
+      b.goff = a.goff; b.glen = a.glen; b.ub = a.ub; b.ucoef = a.ucoef; b.ubop = a.ubop;
+      b.coef = DBuf::view(a.coef);
+      b.bop = DBuf::view(a.bop);
+      if (L > 1 || l == 0) {
+        b.u.alloc(b.geo.total * vsize(l), s);
+        b.f.alloc(b.geo.total * vsize(l), s);
+        b.r_.alloc(b.geo.total * vsize(l), s);
+      }
+    }
+    c->io.alloc(io.bytes, s);
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    CK(cudaEventCreateWithFlags(&c->ev_dots, cudaEventDisableTiming));
+    CK(cudaMallocHost((void **)&c->hpin, 4096 * sizeof(double)));
+    CK(cudaStreamSynchronize(s));
+    return std::unique_ptr<SolverBase>(c.release());
+  }
+
   // ------------------------------------------------------------ introspection
   int64_t level_nodes(int l, int64_t n[3]) const override {
     if (l < 0 || l >= L) return -1;
@@ -2033,8 +2110,35 @@ template <typename T> struct Solver : SolverBase {
 }  // namespace hmg
 
 // =====================================================================  C-ABI
+// One hierarchy, one workspace per stream ("the library allocates one
+// workspace per stream on first use, keyed by the stream"): the first stream that runs
+// a call uses the build's solver; every other stream gets a clone sharing the
+// coefficients (clone_workspace).  Calls on one stream are serialised by the caller;
+// calls on different streams may run concurrently from different host threads.
+// Partitioned hierarchies serve one stream (their collectives must match across ranks).
 struct hmg_hierarchy {
   std::unique_ptr<hmg::SolverBase> impl;
+  mutable std::mutex mu;
+  mutable bool claimed = false;
+  mutable void *first = nullptr;
+  mutable std::map<void *, std::unique_ptr<hmg::SolverBase>> per_stream;
+  ~hmg_hierarchy() { per_stream.clear(); }   // clones (views) before the owner
+  hmg::SolverBase *ws(void *stream) const {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!claimed) {
+      claimed = true;
+      first = stream;
+    }
+    if (stream == first) return impl.get();
+    auto it = per_stream.find(stream);
+    if (it != per_stream.end()) return it->second.get();
+    if (impl->comm && impl->comm->size > 1)
+      throw hmg::HmgError(HMG_EINVAL, "a partitioned hierarchy serves one stream");
+    auto c = impl->clone_workspace(reinterpret_cast<cudaStream_t>(stream));
+    hmg::SolverBase *r = c.get();
+    per_stream.emplace(stream, std::move(c));
+    return r;
+  }
 };
 
 struct hmg_comm {
@@ -2247,7 +2351,7 @@ static hmg_status build_impl(const hmg_options *o, const double *kappa, double o
 hmg_status hmg_apply_helmholtz(const hmg_hierarchy *h, int level, int shifted, const void *x, void *y, void *stream) {
   HMG_API_BEGIN
   if (!h || !x || !y) return fail(HMG_EINVAL, "null pointer");
-  h->impl->api_apply(level, shifted, x, y, S(stream));
+  h->ws(stream)->api_apply(level, shifted, x, y, S(stream));
   return HMG_OK;
   HMG_API_END
 }
@@ -2256,7 +2360,7 @@ hmg_status hmg_residual(const hmg_hierarchy *h, int level, int shifted, const vo
                         void *stream) {
   HMG_API_BEGIN
   if (!h || !f || !x || !r) return fail(HMG_EINVAL, "null pointer");
-  h->impl->api_residual(level, shifted, f, x, r, S(stream));
+  h->ws(stream)->api_residual(level, shifted, f, x, r, S(stream));
   return HMG_OK;
   HMG_API_END
 }
@@ -2264,7 +2368,7 @@ hmg_status hmg_residual(const hmg_hierarchy *h, int level, int shifted, const vo
 hmg_status hmg_smooth(const hmg_hierarchy *h, int level, const void *f, void *u, void *stream) {
   HMG_API_BEGIN
   if (!h || !f || !u) return fail(HMG_EINVAL, "null pointer");
-  h->impl->api_smooth(level, f, u, S(stream));
+  h->ws(stream)->api_smooth(level, f, u, S(stream));
   return HMG_OK;
   HMG_API_END
 }
@@ -2272,7 +2376,7 @@ hmg_status hmg_smooth(const hmg_hierarchy *h, int level, const void *f, void *u,
 hmg_status hmg_restrict(const hmg_hierarchy *h, int level, const void *r, void *fc, void *stream) {
   HMG_API_BEGIN
   if (!h || !r || !fc) return fail(HMG_EINVAL, "null pointer");
-  h->impl->api_restrict(level, r, fc, S(stream));
+  h->ws(stream)->api_restrict(level, r, fc, S(stream));
   return HMG_OK;
   HMG_API_END
 }
@@ -2280,7 +2384,7 @@ hmg_status hmg_restrict(const hmg_hierarchy *h, int level, const void *r, void *
 hmg_status hmg_prolong_add(const hmg_hierarchy *h, int level, const void *ec, void *u, void *stream) {
   HMG_API_BEGIN
   if (!h || !ec || !u) return fail(HMG_EINVAL, "null pointer");
-  h->impl->api_prolong(level, ec, u, S(stream));
+  h->ws(stream)->api_prolong(level, ec, u, S(stream));
   return HMG_OK;
   HMG_API_END
 }
@@ -2288,7 +2392,7 @@ hmg_status hmg_prolong_add(const hmg_hierarchy *h, int level, const void *ec, vo
 hmg_status hmg_coarse_solve(const hmg_hierarchy *h, const void *r, void *e, void *stream) {
   HMG_API_BEGIN
   if (!h || !r || !e) return fail(HMG_EINVAL, "null pointer");
-  h->impl->api_coarse(r, e, S(stream));
+  h->ws(stream)->api_coarse(r, e, S(stream));
   return HMG_OK;
   HMG_API_END
 }
@@ -2296,7 +2400,7 @@ hmg_status hmg_coarse_solve(const hmg_hierarchy *h, const void *r, void *e, void
 hmg_status hmg_vcycle(const hmg_hierarchy *h, const void *f, void *x, int x_is_zero, void *stream) {
   HMG_API_BEGIN
   if (!h || !f || !x) return fail(HMG_EINVAL, "null pointer");
-  h->impl->api_vcycle(f, x, x_is_zero, S(stream));
+  h->ws(stream)->api_vcycle(f, x, x_is_zero, S(stream));
   return HMG_OK;
   HMG_API_END
 }
@@ -2305,7 +2409,7 @@ hmg_status hmg_fgmres_solve(const hmg_hierarchy *h, const void *q, void *x, int 
                             void *stream, hmg_report *rep) {
   HMG_API_BEGIN
   if (!h || !q || !x) return fail(HMG_EINVAL, "null pointer");
-  hmg_status st = h->impl->api_fgmres(q, x, 0, restart, tol, maxiter, S(stream), rep);
+  hmg_status st = h->ws(stream)->api_fgmres(q, x, 0, restart, tol, maxiter, S(stream), rep);
   if (st == HMG_ENOTCONVERGED) t_err = "FGMRES reached maxiter without converging";
   return st;
   HMG_API_END
@@ -2315,7 +2419,7 @@ hmg_status hmg_fgmres_solve_host(const hmg_hierarchy *h, const void *q, void *x,
                                  int maxiter, void *stream, hmg_report *rep) {
   HMG_API_BEGIN
   if (!h || !q || !x) return fail(HMG_EINVAL, "null pointer");
-  hmg_status st = h->impl->api_fgmres(q, x, 1, restart, tol, maxiter, S(stream), rep);
+  hmg_status st = h->ws(stream)->api_fgmres(q, x, 1, restart, tol, maxiter, S(stream), rep);
   if (st == HMG_ENOTCONVERGED) t_err = "FGMRES reached maxiter without converging";
   return st;
   HMG_API_END
@@ -2325,7 +2429,7 @@ hmg_status hmg_fgmres_solve_batch(const hmg_hierarchy *h, int nrhs, const void *
                                   int maxiter, void *stream, hmg_report *reps) {
   HMG_API_BEGIN
   if (!h || !q || !x) return fail(HMG_EINVAL, "null pointer");
-  hmg_status st = h->impl->api_fgmres_batch(nrhs, q, x, 0, restart, tol, maxiter, S(stream), reps);
+  hmg_status st = h->ws(stream)->api_fgmres_batch(nrhs, q, x, 0, restart, tol, maxiter, S(stream), reps);
   if (st == HMG_ENOTCONVERGED) t_err = "FGMRES reached maxiter without converging for at least one right-hand side";
   return st;
   HMG_API_END

@@ -411,7 +411,11 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
 // loop and predicate logic) is shared by the two nodes.
 constexpr int RB2_STRIP = 56;
 
-template <int KIND, bool ZERO, int SEG, typename TR, int MINB, int PD, int UNR = 1>
+// MODE 0: every warp, generic.  MODE 1: only the warps whose whole footprint (columns of the
+// strip, rows y0-4 .. y0+SEG+4) lies inside the uniform box and one node inside the domain,
+// with sigma, ia, id, the patch count (4) and the masks as constants -- the same operations on
+// the same values as the generic code, so bit-identical.  MODE 2: the remaining warps, generic.
+template <int KIND, bool ZERO, int SEG, typename TR, int MINB, int PD, int UNR = 1, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *__restrict__ sig,
                                                            const float2 *__restrict__ ia_,
                                                            const float2 *__restrict__ id_, double alpha_d,
@@ -431,22 +435,31 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
   if (y0 >= g.n[1]) return;
   const int y1 = min(g.n[1], y0 + SEG);
   const int x0 = strip * RB2_STRIP - 4 + 2 * lane;   // this lane's columns x0 (node 0) and x0 + 1 (node 1)
+  if (MODE != 0) {
+    const int xa = strip * RB2_STRIP - 4, xb = strip * RB2_STRIP + 60, ya = y0 - 4, yb = y0 + SEG + 4;
+    const bool inner = xa >= ub.lo[0] && xb <= ub.hi[0] && ya >= ub.lo[1] && yb <= ub.hi[1] &&
+                       xa + g.o[0] >= 1 && xb + g.o[0] <= g.N[0] - 1 && ya + g.o[1] >= 1 && yb + g.o[1] <= g.N[1] - 1;
+    if (inner != (MODE == 1)) return;
+  }
+  constexpr bool FAST = MODE == 1;
   const bool out_lane = lane >= 2 && lane < 30;
   bool outn[2], xin[2];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     outn[q] = out_lane && x0 + q < g.n[0];
-    xin[q] = x0 + q + g.o[0] >= 0 && x0 + q + g.o[0] < g.N[0];
+    xin[q] = FAST || (x0 + q + g.o[0] >= 0 && x0 + q + g.o[0] < g.N[0]);
   }
   const D e = W::Le * ih2;
   const CD z = mkc<D>(0, 0);
   const CS zs = mkc<float>(0, 0);
   // rows clamped to y1 + 2 as in k_rb2d_march (beyond it: possibly past this rank's box)
   const int ylo = -g.o[1], yhi = min(g.N[1] - g.o[1], y1 + 3), ydom = g.N[1] - g.o[1];
-  auto yok = [&](int y) { return y >= ylo && y < yhi; };
+  auto yok = [&](int y) { return FAST || (y >= ylo && y < yhi); };
   // uniform box (k_uniform.cuh): both columns inside -> sigma, ia, id of row y from the box's copies
   const bool xuni = x0 >= ub.lo[0] && x0 + 1 < ub.hi[0];
-  auto urow = [&](int y) { return xuni && y >= ub.lo[1] && y < ub.hi[1]; };
+  auto urow = [&](int y) { return FAST || (xuni && y >= ub.lo[1] && y < ub.hi[1]); };
+  const CD uia_d = ccast<D, float>(uia), uid_d = ccast<D, float>(uid);   // (FAST: the constants in fp64)
+  const D wcnt4 = w * (D)kRbInvCnt[4];
   CS um1[2] = {zs, zs}, u0[2] = {zs, zs}, up1[2] = {zs, zs}, ub1[2] = {zs, zs};
   CD r2[2] = {z, z}, r1[2] = {z, z}, r0[2] = {z, z};
   CD h2[2] = {z, z}, h1[2] = {z, z}, h0[2] = {z, z};
@@ -551,7 +564,7 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
     for (int q = 0; q < 2; ++q) {
       r2[q] = r1[q]; r1[q] = r0[q]; r0[q] = rb[q];
       a2[q] = a1[q]; a1[q] = a0[q]; a0[q] = av[q];
-      t0[q] = cmul<D>(rb[q], ccast<D, float>(av[q]));
+      t0[q] = cmul<D>(rb[q], FAST ? uia_d : ccast<D, float>(av[q]));
       h2[q] = h1[q]; h1[q] = h0[q];
     }
     h0[0] = cadd<D>(shfl_up1(t0[1]), t0[1]);
@@ -561,7 +574,7 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
     for (int q = 0; q < 2; ++q) {
       const CD sdiag = cadd<D>(h2[q], h0[q]);
       const CD num = mkc<D>(r1[q].x - e * sdiag.x, r1[q].y - e * sdiag.y);
-      yc[q] = (xin[q] && yok(b - 1)) ? cmul<D>(num, ccast<D, float>(dv[q])) : z;
+      yc[q] = (xin[q] && yok(b - 1)) ? cmul<D>(num, FAST ? uid_d : ccast<D, float>(dv[q])) : z;
       c2[q] = c1[q]; c1[q] = yc[q];
       g3[q] = g2[q]; g2[q] = g1[q];
     }
@@ -573,13 +586,21 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const CD syl = cadd<D>(g3[q], g1[q]);
-        const int xq = x0 + q + g.o[0];
-        const bool xm = xq - 1 >= 0, xp = xq + 1 < g.N[0];
-        const bool ym = yo - 1 >= ylo, yp = yo + 1 < ydom;
-        const int k = (int)(xm && ym) + (int)(xp && ym) + (int)(xm && yp) + (int)(xp && yp);
-        const D kd = (D)kRbCount[k];
-        const CD lv = cmul<D>(mkc<D>(kd * r2[q].x - e * syl.x, kd * r2[q].y - e * syl.y), ccast<D, float>(a2[q]));
-        const CD upd = cscale<D>(cadd<D>(c2[q], lv), w * (D)kRbInvCnt[k]);
+        D kd, wc;
+        if (FAST) {   // interior: all four diagonal anchors present
+          kd = 4.0;
+          wc = wcnt4;
+        } else {
+          const int xq = x0 + q + g.o[0];
+          const bool xm = xq - 1 >= 0, xp = xq + 1 < g.N[0];
+          const bool ym = yo - 1 >= ylo, yp = yo + 1 < ydom;
+          const int k = (int)(xm && ym) + (int)(xp && ym) + (int)(xm && yp) + (int)(xp && yp);
+          kd = (D)kRbCount[k];
+          wc = w * (D)kRbInvCnt[k];
+        }
+        const CD lv = cmul<D>(mkc<D>(kd * r2[q].x - e * syl.x, kd * r2[q].y - e * syl.y),
+                              FAST ? uia_d : ccast<D, float>(a2[q]));
+        const CD upd = cscale<D>(cadd<D>(c2[q], lv), wc);
         o[q] = ccast<float, D>(ZERO ? upd : cadd<D>(ccast<D, float>(ub1[q]), upd));
       }
       float2 *dst = u_out + (ob - 2 * px);

@@ -8,6 +8,8 @@ oracle takes minutes, so its results are stored instead of recomputed:
   config3_n128  : configs[3] family at 128^3 cells, 5 levels, alpha 0.5, FGMRES(10)
   config4_s4    : configs[4] generator at 1/4 scale (192 x 192 x 96 cells, h = 100 m),
                   5 levels, alpha 0.5, FGMRES(20)  (SURVEY §8(d) replica)
+  config4_s4_a06: the same replica with alpha 0.6, the shift frozen for config 4 by the
+                  1/2-scale sweep (profiles/r02_config4_sweep.jsonl, reading R16)
 
 Checked, through the C-ABI: the input SHA-256 (same seeded problem); one V-cycle of
 the source at 261 sampled nodes (c128 1e-10 / c64 1e-4 of max|z|, the V-cycle bar of
@@ -57,6 +59,7 @@ def _vals(rec):
     ("config1_n1024", "c64"), ("config1_n1024", "c128"),
     ("config3_n128", "c64"), ("config3_n128", "c128"),
     ("config4_s4", "c64"), ("config4_s4", "c128"),
+    ("config4_s4_a06", "c64"),
 ])
 def test_golden(name, dtype):
     import torch

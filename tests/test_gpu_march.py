@@ -60,3 +60,35 @@ def test_march_bit_identical(monkeypatch, medium, cells, stencil):
     rb = gb.fgmres_solve(q, xb, restart=10, tol=1e-6, maxiter=300)
     assert ra.iterations == rb.iterations and ra.history == rb.history
     assert torch.equal(xa, xb)
+
+
+@pytest.mark.parametrize("n", [256, 304])
+def test_rb_fast_path_bit_identical(monkeypatch, n):
+    """The RB sweep's constant-coefficient instance for warps inside the uniform box (MODE 1 of
+    k_rb2d_march2) against the generic instance everywhere (HMG_NO_RB_FAST=1): bit-identical
+    smoothing steps, V-cycles and FGMRES solves (config-1 family, c64)."""
+    import torch
+    from paper_2511_16808_b200 import hmg, media
+    p = media.config_problem(1, n=n) if n == 256 else media.homogeneous_problem(2, n, sponge=16)
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=4, smoother="rb", damping=DAMPING[(2, "rb")], dtype="c64")
+    monkeypatch.delenv("HMG_NO_RB_FAST", raising=False)
+    ga = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.25)
+    monkeypatch.setenv("HMG_NO_RB_FAST", "1")
+    gb = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.25)
+    monkeypatch.delenv("HMG_NO_RB_FAST")
+    assert ga.uniform_box(0)[0] > 0
+    f = torch.from_numpy(media.random_complex(p.n, 2)).to(torch.complex64).cuda()
+    u = torch.from_numpy(media.random_complex(p.n, 3)).to(torch.complex64).cuda()
+    ua, ub = u.clone(), u.clone()
+    ga.smooth(f, ua)
+    gb.smooth(f, ub)
+    assert torch.equal(ua, ub)
+    q = torch.from_numpy(p.q.ravel()).to(torch.complex64).cuda()
+    za, zb = torch.zeros_like(q), torch.zeros_like(q)
+    ga.vcycle(q, za)
+    gb.vcycle(q, zb)
+    assert torch.equal(za, zb)
+    xa, xb = torch.zeros_like(q), torch.zeros_like(q)
+    ra = ga.fgmres_solve(q, xa, restart=20, tol=1e-6, maxiter=400)
+    rb = gb.fgmres_solve(q, xb, restart=20, tol=1e-6, maxiter=400)
+    assert ra.iterations == rb.iterations and torch.equal(xa, xb)

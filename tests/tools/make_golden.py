@@ -39,6 +39,8 @@ CASES = {
     # configs[4] generator (seed 4) at 1/4 scale: 192 x 192 x 96 cells, h = 100 m, 5 levels
     # (SURVEY §8(d) "full parity on a scaled replica ... 192x192x96 cells, h = 100 m, 5 levels")
     "config4_s4": (dict(cfg=4, scale=4), 5, 0.5, 20, "element", EL3),
+    # the same replica with the shift frozen for config 4 by the 1/2-scale sweep (reading R16)
+    "config4_s4_a06": (dict(cfg=4, scale=4), 5, 0.6, 20, "element", EL3),
 }
 
 
