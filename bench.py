@@ -219,16 +219,21 @@ def run_ours(args):
     per_launch_bytes = top["bytes"] / top["launches"]
     avg_ms = top["ms"] / top["launches"]
     achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_ratio = None, None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(f"{top_name}|{args.dtype}|{n}")
+        tj = json.load(open(tf))
+        traffic = tj.get(f"{top_name}|{args.dtype}|{n}")
+        traffic_ratio = tj.get(f"{top_name}|{args.dtype}|{n}|ratio")
     table = {k: {"launches": v["launches"], "ms_total": round(v["ms"], 3),
                  "share": round(v["ms"] / tot_ms, 4) if tot_ms else None,
                  "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 else None}
              for k, v in kern}
     roofline = {"bound": "hbm", "kernel": top_name, "achieved": round(achieved, 1), "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json: mean ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                                  "per launch over one restart cycle's launches (ncu --set full)",
+                "traffic_over_algorithmic": traffic_ratio,
                 "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_ms,
                 "share_of_step": round(top["ms"] / tot_ms, 4) if tot_ms else None}
     # whole-solve modelled HBM fraction: algorithmic bytes of every kernel / device time

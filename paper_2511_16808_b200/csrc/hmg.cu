@@ -352,6 +352,7 @@ template <typename T> struct Solver : SolverBase {
   bool stage3d = true;    // 3D fine operator: z-marching staged kernel (HMG_NO_STAGE3D=1 at build: the gather)
   bool fmarch = true;     // 2D c64 fine operator: warp-marching kernel (HMG_NO_FMARCH=1 at build: node-parallel)
   bool rbfast = true;     // RB sweep: constant-coefficient interior warps (HMG_NO_RB_FAST=1 at build: generic)
+  int vanka_bz = 2;       // assembled-Vanka stencil: nodes per thread along the slow axis (HMG_VANKA_BZ at build)
   DBuf rb_ia, rb_id;      // its sigma-only factors 1/a_j and 1/(a_c - e^2 sum 1/a_l), stored in T
   C usig{}, uia{}, uid{};  // level-0 uniform-box values of sig, rb_ia, rb_id
   D usigd{};
@@ -405,6 +406,7 @@ template <typename T> struct Solver : SolverBase {
     stage3d = std::getenv("HMG_NO_STAGE3D") == nullptr;
     fmarch = std::getenv("HMG_NO_FMARCH") == nullptr;
     rbfast = std::getenv("HMG_NO_RB_FAST") == nullptr;
+    vanka_bz = std::getenv("HMG_VANKA_BZ") ? std::atoi(std::getenv("HMG_VANKA_BZ")) : 2;
     if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
     lev.resize(L);
     int64_t nodes[3] = {opt.cells[0] + 1, opt.cells[1] + 1, dim == 3 ? opt.cells[2] + 1 : 1};
@@ -1239,6 +1241,22 @@ template <typename T> struct Solver : SolverBase {
              (TV *)u, (BV)damp(l), zero, Lv.ub, ucopy<27, BV>(Lv.ubop));
       return;
     }
+    // one right-hand side on a large level: BZ nodes along the slow axis per thread
+    const int vbz = vanka_bz;
+    const int nslow = DIM == 3 ? Lv.geo.n[2] : Lv.geo.n[1];
+    if (nbat(l) == 1 && vbz > 1 && nslow >= 64) {
+      tag(zero ? "vanka_zero" : "vanka", l, (double)NB * sizeof(C) * outside(l) + (zero ? 2 : 3) * sizeof(TV) * nn);
+      auto go = [&](auto kern, int bz) {
+        dim3 grid = nl.grid;
+        if (DIM == 3) grid.z = (Lv.geo.n[2] + bz - 1) / bz;
+        else grid.y = (Lv.geo.n[1] + 8 * bz - 1) / (8 * bz);
+        launch(kern, grid, nl.block, 0, s, Lv.geo, (const C *)Lv.bop.template as<C>(), (const TV *)r, (const TV *)u,
+               (TV *)u, (BV)damp(l), zero, Lv.ub, ucopy<NB, BV>(Lv.ubop));
+      };
+      if (vbz >= 4) go(k_vanka_stencil_blk<BV, T, DIM, KIND, 4>, 4);
+      else go(k_vanka_stencil_blk<BV, T, DIM, KIND, 2>, 2);
+      return;
+    }
     over_batch(nbat(l), [&](auto NRc, int q0) {
       constexpr int NR = decltype(NRc)::value;
       tag(zero ? "vanka_zero" : "vanka", l, (double)NB * sizeof(C) * outside(l) + (zero ? 2 : 3) * sizeof(TV) * NR * nn);
@@ -2033,6 +2051,7 @@ template <typename T> struct Solver : SolverBase {
     c->stage3d = stage3d;
     c->fmarch = fmarch;
     c->rbfast = rbfast;
+    c->vanka_bz = vanka_bz;
     c->usig = usig; c->uia = uia; c->uid = uid; c->usigd = usigd;
     c->sig = DBuf::view(sig);
     c->sigd = DBuf::view(sigd);

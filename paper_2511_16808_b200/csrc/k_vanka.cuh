@@ -175,6 +175,65 @@ __global__ void __launch_bounds__(256) k_vanka_stencil(Geo g, const cplx<TK> *__
   }
 }
 
+// Register-blocked k_vanka_stencil (one right-hand side): each thread owns BZ consecutive
+// nodes along the slowest axis (y in 2D, z in 3D) so every r value is loaded once for all
+// the outputs it reaches; input rows / planes are visited in increasing order and each
+// output takes its offsets p in increasing order -- the arithmetic of k_vanka_stencil.
+template <typename T, typename TK, int DIM, int KIND, int BZ>
+__global__ void __launch_bounds__(256) k_vanka_stencil_blk(Geo g, const cplx<TK> *__restrict__ B,
+                                                           const cplx<T> *__restrict__ r, const cplx<T> *u,
+                                                           cplx<T> *u_out, T w, int zero, UBox ub,
+                                                           UCoef<BStencil<DIM, KIND>::NB, T> uc) {
+  using S = BStencil<DIM, KIND>;
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iyt = blockIdx.y * blockDim.y + threadIdx.y;
+  const int iy = DIM == 3 ? iyt : iyt * BZ;
+  const int iz = DIM == 3 ? blockIdx.z * BZ : 0;
+  if (ix >= g.n[0] || iy >= g.n[1] || iz >= g.n[2]) return;
+  const int64_t j0 = g.idx(ix, iy, iz);
+  const int64_t ps = DIM == 3 ? g.pxy : g.px;
+  const int slow0 = DIM == 3 ? iz : iy, nslow = DIM == 3 ? g.n[2] : g.n[1];
+  const int olast = min(slow0 + BZ, nslow) - 1 - slow0;
+  const bool uni = DIM == 3 ? ub.in(ix, iy, iz) && ub.in(ix, iy, iz + olast)
+                            : ub.in(ix, iy, 0) && ub.in(ix, iy + olast, 0);
+  constexpr int SR = 2;   // |slow offset| <= 2 for every patch kind
+  cplx<T> acc[BZ];
+#pragma unroll
+  for (int o = 0; o < BZ; ++o) acc[o] = mkc<T>(0, 0);
+  auto run = [&](auto bcoef) {
+#pragma unroll
+    for (int sl = -SR; sl < BZ + SR; ++sl) {
+      if (sl > olast + SR) break;
+#pragma unroll
+      for (int o = 0; o < BZ; ++o) {
+        static_for<0, S::NB>([&](auto P) {
+          constexpr int p = decltype(P)::value;
+          constexpr int sp = DIM == 3 ? S::template dz<p> : S::template dy<p>;
+          if (sp != sl - o) return;
+          const int64_t a = j0 + (int64_t)sl * ps + (DIM == 3 ? (int64_t)S::template dy<p> * g.px : 0) +
+                            S::template dx<p>;
+          acc[o] = cfma<T>(acc[o], bcoef(p, o), r[a]);
+        });
+      }
+    }
+  };
+  if (uni) run([&](int p, int) { return uc.c[p]; });
+  else run([&](int p, int o) { return ccast<T, TK>(B[(int64_t)p * g.total + j0 + (int64_t)o * ps]); });
+#pragma unroll
+  for (int o = 0; o < BZ; ++o) {
+    if (o > olast) break;
+    const int64_t j = j0 + (int64_t)o * ps;
+    cplx<T> v;
+    if (zero) {
+      v = mkc<T>(__fmul_rn_t(acc[o].x, w), __fmul_rn_t(acc[o].y, w));
+    } else {
+      const cplx<T> uq = u[j];
+      v = mkc<T>(fma(acc[o].x, w, uq.x), fma(acc[o].y, w, uq.y));
+    }
+    u_out[j] = v;
+  }
+}
+
 // (1b) fine-level RB smoothing sweep in ONE kernel (2D, matrix-free).
 // With the compact stencil the RB patch matrix is an arrow: leaf-leaf entries
 // vanish (offsets (2,0), (2,2) lie outside the 9-point support), centre-leaf =

@@ -104,10 +104,13 @@ def full(src, dst, traffic_key=None, traffic_kernel=None):
     if traffic_key:
         tf = os.path.join(os.path.dirname(dst), "ncu_traffic.json")
         cur = json.load(open(tf)) if os.path.exists(tf) else {}
+        # mean DRAM read+write bytes per captured launch of the matching kernel (the roofline's
+        # `achieved` is an average over launches too)
         cand = [v for k, v in traffic.items() if not traffic_kernel or traffic_kernel in k]
-        best = max(cand, key=lambda v: max(v)) if cand else None
-        if best:
-            cur[traffic_key] = max(best)
+        allv = [x for v in cand for x in v]
+        if allv:
+            cur[traffic_key] = sum(allv) / len(allv)
+            cur[traffic_key + "|launches"] = len(allv)
         json.dump(cur, open(tf, "w"), indent=1)
 
 
