@@ -353,6 +353,9 @@ template <typename T> struct Solver : SolverBase {
   bool fmarch = true;     // 2D c64 fine operator: warp-marching kernel (HMG_NO_FMARCH=1 at build: node-parallel)
   bool rbfast = true;     // RB sweep: constant-coefficient interior warps (HMG_NO_RB_FAST=1 at build: generic)
   int vanka_bz = 2;       // assembled-Vanka stencil: nodes per thread along the slow axis (HMG_VANKA_BZ at build)
+  int smarch = 0;         // 2D c64 stored stencil: warp-marching kernel on large levels, segment height
+                          // (HMG_SMARCH=8|16 at build; off by default: measured slower than the blocked gather)
+  bool rrfuse = true;     // 2D c64 fine residual + restriction fused (HMG_NO_RRFUSE=1 at build)
   DBuf rb_ia, rb_id;      // its sigma-only factors 1/a_j and 1/(a_c - e^2 sum 1/a_l), stored in T
   C usig{}, uia{}, uid{};  // level-0 uniform-box values of sig, rb_ia, rb_id
   D usigd{};
@@ -406,7 +409,11 @@ template <typename T> struct Solver : SolverBase {
     stage3d = std::getenv("HMG_NO_STAGE3D") == nullptr;
     fmarch = std::getenv("HMG_NO_FMARCH") == nullptr;
     rbfast = std::getenv("HMG_NO_RB_FAST") == nullptr;
-    vanka_bz = std::getenv("HMG_VANKA_BZ") ? std::atoi(std::getenv("HMG_VANKA_BZ")) : 2;
+    smarch = std::getenv("HMG_SMARCH") ? std::atoi(std::getenv("HMG_SMARCH")) : 0;
+    rrfuse = std::getenv("HMG_NO_RRFUSE") == nullptr;
+    // measured: BZ = 2 helps the 3D element operator (config 3 level 0: 53 -> 50 ms per solve)
+    // and hurts the 2D RB one (level 1 at N = 4096: 103 -> 117 ms)
+    vanka_bz = std::getenv("HMG_VANKA_BZ") ? std::atoi(std::getenv("HMG_VANKA_BZ")) : (opt.dim == 3 ? 2 : 1);
     if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
     lev.resize(L);
     int64_t nodes[3] = {opt.cells[0] + 1, opt.cells[1] + 1, dim == 3 ? opt.cells[2] + 1 : 1};
@@ -985,6 +992,31 @@ template <typename T> struct Solver : SolverBase {
     return true;
   }
 
+  // f_c = R_0 (f - H_s u) in ONE warp-marching kernel (2D c64 fine level with the bicubic
+  // fine restriction, one rank); false: not applicable (separate residual + restriction)
+  bool resrestrict(int l, const void *u, const void *f, void *fc, cudaStream_t s) {
+    if (l != 0 || !rrfuse || !std::is_same<T, float>::value || opt.dim != 2 || (G % 2) != 0 || lev[0].rR != 2 ||
+        nbat(0) != 1 || (comm && comm->size > 1) || lev[1].gather_in)
+      return false;
+    const Geo &g = lev[0].geo, &gc = lev[1].geo;
+    constexpr int SEG = 32, PD = 2, NST = PD + 2;
+    const int nstrips = (g.n[0] + RR_STRIP - 1) / RR_STRIP, nsegs = (g.n[1] + SEG - 1) / SEG;
+    const int64_t warps = (int64_t)nstrips * nsegs;
+    const dim3 grid((unsigned)((warps + 3) / 4)), block(128);
+    const int smem = 4 * NST * 3 * 32 * 16;
+    const double ih2 = 1.0 / (lev[0].h * lev[0].h);
+    const double nn = (double)g.nodes();
+    tag("residual_restrict", 0, 2.0 * sizeof(C) * nn + sizeof(C) * outside(0) + 16.0 * gc.nodes());
+    auto go = [&](auto kern) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      launch(kern, grid, block, (size_t)smem, s, g, gc, (const float2 *)sig.template as<C>(), alpha, ih2,
+             (const float2 *)u, (const float2 *)f, (double2 *)fc, lev[0].ub, widen(usig));
+    };
+    if (opt.fine_stencil == HMG_COMPACT4) go(k_fine_resrestrict2d_march<ST_COMPACT4, SEG, PD>);
+    else go(k_fine_resrestrict2d_march<ST_FD2, SEG, PD>);
+    return true;
+  }
+
   // 3D fine operator y = A x / y = f - A x: the z-marching staged kernel (k_stage3d.cuh)
   // or the node-parallel gather (bit-identical; HMG_NO_STAGE3D=1)
   template <typename TT, typename TC, typename TS>
@@ -1095,6 +1127,26 @@ template <typename T> struct Solver : SolverBase {
         std::getenv("HMG_NO_PAIR_ST") == nullptr) {   // two nodes per thread, 16-byte coefficient pairs
       tag(f ? "stored_residual" : "stored_apply", l, kcount(opt.dim, Lv.r) * sizeof(C) * outside(l) + (f ? 3 : 2) * sz * nn);
       const float2 *c2 = reinterpret_cast<const float2 *>(cf);
+      if (smarch > 0 && Lv.geo.n[1] >= 256) {   // warp-marching version on the large levels (opt-in)
+        constexpr int PD = 2;
+        const int SEG = smarch;
+        const int nstrips = (Lv.geo.n[0] + SM_STRIP - 1) / SM_STRIP, nsegs = (Lv.geo.n[1] + SEG - 1) / SEG;
+        const int64_t warps = (int64_t)nstrips * nsegs;
+        const dim3 grid((unsigned)((warps + 3) / 4)), block(128);
+        const int smem = 4 * (PD + 2) * 2 * 32 * 16;
+        auto gom = [&](auto kern, auto ucp) {
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          launch(kern, grid, block, (size_t)smem, s, Lv.geo, c2, xx, ff, yy, Lv.ub, ucp);
+        };
+        if (Lv.r == 1) {
+          if (SEG == 8) gom(k_stored_op2d_march<1, 8, PD>, ucopy<9, double>(Lv.ucoef));
+          else gom(k_stored_op2d_march<1, 16, PD>, ucopy<9, double>(Lv.ucoef));
+        } else {
+          if (SEG == 8) gom(k_stored_op2d_march<2, 8, PD>, ucopy<25, double>(Lv.ucoef));
+          else gom(k_stored_op2d_march<2, 16, PD>, ucopy<25, double>(Lv.ucoef));
+        }
+        return;
+      }
       // BY output rows per thread (register blocking) on the large levels, 1 on small ones (parallelism)
       static const int by_env = std::getenv("HMG_STORED_BY") ? std::atoi(std::getenv("HMG_STORED_BY")) : 2;
       const int BY = Lv.geo.n[1] >= 512 ? by_env : 1;
@@ -1470,9 +1522,11 @@ template <typename T> struct Solver : SolverBase {
       else smooth_inplace(l, f, u, s);
     }
     if (opt.nu1 == 0 && zero) CK(cudaMemsetAsync(u, 0, Lv.geo.total * vsize(l) * nbat(l), s));
-    op(l, 1, u, f, Lv.r_.p, s);                                // step 2: r = f - A u
     Level &Cc = lev[l + 1];
-    restrict_(l, Lv.r_.p, Cc.f.p, s);                          //         f_c = R r
+    if (!resrestrict(l, u, f, Cc.f.p, s)) {                    // step 2 fused (2D c64 fine level), else:
+      op(l, 1, u, f, Lv.r_.p, s);                              //   r = f - A u
+      restrict_(l, Lv.r_.p, Cc.f.p, s);                        //   f_c = R r
+    }
     const int rec = opt.cycle == 1 ? 2 : 1;                    // step 3: V / W recursion
     for (int c = 0; c < rec; ++c) cycle(l + 1, Cc.f.p, Cc.u.p, c == 0, s, capturing);
     if (opt.nu2 > 0 && fused_sweep(l)) {
@@ -2052,6 +2106,8 @@ template <typename T> struct Solver : SolverBase {
     c->fmarch = fmarch;
     c->rbfast = rbfast;
     c->vanka_bz = vanka_bz;
+    c->smarch = smarch;
+    c->rrfuse = rrfuse;
     c->usig = usig; c->uia = uia; c->uid = uid; c->usigd = usigd;
     c->sig = DBuf::view(sig);
     c->sigd = DBuf::view(sigd);

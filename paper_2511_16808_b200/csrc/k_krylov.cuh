@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(KRY_THREADS) k_scale(const cplx<TI> *__restric
 // c64 variants: two complex values per 16-byte load (float4).  Slab offsets,
 // lengths and the vector stride are multiples of 8 elements (row pitch
 // rounded to 8), so every pair is 16-byte aligned.  len2 = len / 2 pairs.
-template <int NV, bool SELF>
+template <int NV, bool SELF, int U = 1>
 __global__ void __launch_bounds__(KRY_THREADS) k_multidot_f4(const float4 *__restrict__ V, int64_t vstride2,
                                                              const float4 *__restrict__ w, int64_t len2,
                                                              double2 *__restrict__ partial) {
@@ -173,11 +173,9 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multidot_f4(const float4 *__res
 #pragma unroll
   for (int i = 0; i < NA; ++i) ar[i] = ai[i] = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len2; e += stride) {
-    float4 v[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = V[(int64_t)i * vstride2 + e];
-    const float4 wv = w[e];
+  // U elements per thread and trip (all their loads issued before the arithmetic); each
+  // thread still accumulates its elements in increasing order: the same sums for any U
+  auto acc = [&](const float4 (&v)[NV], const float4 wv) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       ar[i] = fma((double)v[i].x, (double)wv.x, fma((double)v[i].y, (double)wv.y, ar[i]));
@@ -189,6 +187,26 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multidot_f4(const float4 *__res
       ar[NV] = fma((double)wv.x, (double)wv.x, fma((double)wv.y, (double)wv.y, ar[NV]));
       ar[NV] = fma((double)wv.z, (double)wv.z, fma((double)wv.w, (double)wv.w, ar[NV]));
     }
+  };
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (U == 2) {
+    for (; e + stride < len2; e += 2 * stride) {
+      float4 v0[NV], v1[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        v0[i] = V[(int64_t)i * vstride2 + e];
+        v1[i] = V[(int64_t)i * vstride2 + e + stride];
+      }
+      const float4 w0 = w[e], w1 = w[e + stride];
+      acc(v0, w0);
+      acc(v1, w1);
+    }
+  }
+  for (; e < len2; e += stride) {
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = V[(int64_t)i * vstride2 + e];
+    acc(v, w[e]);
   }
   __shared__ double sr[KRY_THREADS / 32][NA], si[KRY_THREADS / 32][NA];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -206,7 +224,7 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multidot_f4(const float4 *__res
   }
 }
 
-template <int NV, bool NORM>
+template <int NV, bool NORM, int U = 1>
 __global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy_f4(const float4 *__restrict__ V, int64_t vstride2,
                                                                const double2 *__restrict__ coef, const double *vscale,
                                                                double sgn, float4 *__restrict__ w, int64_t len2,
@@ -219,11 +237,8 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy_f4(const float4 *__r
   __syncthreads();
   double nrm = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len2; e += stride) {
-    float4 v[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = V[(int64_t)i * vstride2 + e];
-    const float4 wv = w[e];
+  // U elements per thread and trip, loads first; elements still processed in increasing order
+  auto upd = [&](const float4 (&v)[NV], const float4 wv, int64_t e) {
     double x0 = wv.x, y0 = wv.y, x1 = wv.z, y1 = wv.w;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -239,6 +254,26 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy_f4(const float4 *__r
       nrm = fma((double)o.x, (double)o.x, fma((double)o.y, (double)o.y, nrm));
       nrm = fma((double)o.z, (double)o.z, fma((double)o.w, (double)o.w, nrm));
     }
+  };
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (U == 2) {
+    for (; e + stride < len2; e += 2 * stride) {
+      float4 v0[NV], v1[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        v0[i] = V[(int64_t)i * vstride2 + e];
+        v1[i] = V[(int64_t)i * vstride2 + e + stride];
+      }
+      const float4 w0 = w[e], w1 = w[e + stride];
+      upd(v0, w0, e);
+      upd(v1, w1, e + stride);
+    }
+  }
+  for (; e < len2; e += stride) {
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = V[(int64_t)i * vstride2 + e];
+    upd(v, w[e], e);
   }
   if (NORM) {
     __shared__ double sn[KRY_THREADS / 32];

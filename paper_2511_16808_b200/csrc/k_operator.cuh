@@ -273,6 +273,147 @@ __global__ void __launch_bounds__(128) k_fine_op2d_march(Geo g, const cplx<TSG> 
   }
 }
 
+// Fine-level residual AND bicubic restriction in one warp-marching kernel (2D, c64):
+//   fc = R_0 (f - H_s u)      (Alg. 2.1 step 2; R = bicubic, Eq. 3.2)
+// without writing r.  Strip s: lane l holds the column pair (x0, x0 + 1), x0 = 56 s - 4 + 2 l;
+// the residual is formed (k_fine_op2d_march's arithmetic, rounded to fp32 as the stored r
+// would be) on lanes 1..30 for rows y0 - 2 .. y1 + 1, and the lane holding 2X (lanes
+// 2..29: coarse X in [28 s, 28 s + 28)) restricts it: the x-pass over fine columns 2X-2..2X+2
+// (its own pair and the neighbour lanes' by shuffles), then the y-pass over fine rows
+// 2I-2..2I+2 in rolling accumulators -- the summation order of k_restrict_pair, so fc is
+// bit-identical to the residual kernel followed by k_restrict_pair.  Coarse rows I with
+// 2I in [y0, y1) (y0 even) belong to the segment.
+constexpr int RR_STRIP = 56;
+template <int KIND, int SEG, int PD>
+__global__ void __launch_bounds__(128) k_fine_resrestrict2d_march(Geo g, Geo gc, const float2 *__restrict__ sig,
+                                                                  double alpha, double ih2,
+                                                                  const float2 *__restrict__ x,
+                                                                  const float2 *__restrict__ f,
+                                                                  double2 *__restrict__ fc, UBox ub, double2 us) {
+  using W = FineW<2, KIND>;
+  using CC = double2;
+  static_assert(SEG % 2 == 0, "segments start on even rows");
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nstrips = (g.n[0] + RR_STRIP - 1) / RR_STRIP;
+  const int strip = wid % nstrips, seg = wid / nstrips;
+  const int y0 = seg * SEG;
+  if (y0 >= g.n[1]) return;
+  const int y1 = min(g.n[1], y0 + SEG);
+  const int x0 = strip * RR_STRIP - 4 + 2 * lane;
+  const bool xload = x0 >= -g.G && x0 < g.n[0] + g.G;
+  const bool rlane = lane >= 1 && lane <= 30;
+  // residual columns in the domain (zero outside, as the zero ghost layer of a stored r)
+  const bool in0 = x0 >= 0 && x0 < g.n[0], in1 = x0 + 1 >= 0 && x0 + 1 < g.n[0];
+  const int X = x0 / 2;   // x0 even (x0 >= -4 -> X >= -2)
+  const bool clane = lane >= 2 && lane <= 29 && x0 >= 0 && X < gc.n[0];
+  const bool xuni = x0 >= ub.lo[0] && x0 + 1 < ub.hi[0];
+  auto urow = [&](int yy) { return xuni && yy >= ub.lo[1] && yy < ub.hi[1]; };
+  constexpr int NST = PD + 2, NW = 3;   // x, f, sigma words per lane and row
+  extern __shared__ __align__(16) unsigned char rr_smem[];
+  float4 *ring = reinterpret_cast<float4 *>(rr_smem) + (size_t)(threadIdx.x >> 5) * (NST * NW * 32);
+  const int64_t px = g.px;
+  const int ybeg = y0 - 3;                                   // first input row
+  const int nrows = (y1 + 3) - ybeg;                         // input rows y0-3 .. y1+2
+  const int64_t ob0 = g.base + x0 + (int64_t)ybeg * px;
+  auto cp16 = [&](const void *src, int slot, int k, bool ok) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(ring + (slot * NW + k) * 32 + lane);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(ok ? src : (const void *)x),
+                 "r"(ok ? 16 : 0)
+                 : "memory");
+  };
+  // rows the outputs need: residual rows <= y1 + 1 -> input rows <= y1 + 2 (and inside the box)
+  auto rowok = [&](int b) { return b >= -g.G && b < g.n[1] + g.G; };
+  auto issue = [&](int it) {
+    if (it < nrows) {
+      const int b = ybeg + it, slot = it % NST;
+      const int64_t o = ob0 + (int64_t)it * px;
+      cp16(x + o, slot, 0, xload && rowok(b));
+      const bool dom = b >= 0 && b < g.n[1];
+      cp16(f + o, slot, 1, xload && dom);
+      if (!urow(b) && dom) cp16(sig + o, slot, 2, xload);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int k = 0; k < PD; ++k) issue(k);
+  const CC z = make_double2(0, 0);
+  CC a0 = z, a1 = z, b0 = z, b1 = z, aw = z, ae = z, bw = z, be = z;
+  auto shl = [](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
+  auto shr = [](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
+  CC P = z, Q = z;   // y-pass accumulators of coarse rows I0 - 1 and I0 (see below)
+  const double w2 = 0.0625, w1 = 0.25, w0 = 0.375;   // RW<2>::w(+-2), (+-1), 0
+  for (int it = 0; it < nrows; ++it) {
+    issue(it + PD);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(PD) : "memory");
+    const float4 *sl = ring + (it % NST) * NW * 32 + lane;
+    const float4 xv = sl[0];
+    const CC c0 = make_double2(xv.x, xv.y), c1 = make_double2(xv.z, xv.w);
+    const CC cw = make_double2(shl(c1.x), shl(c1.y)), ce = make_double2(shr(c0.x), shr(c0.y));
+    if (it >= 2) {
+      const int b = ybeg + it - 1;   // residual row (rows a = b-1, b, c = b+1)
+      float2 r0 = make_float2(0, 0), r1 = make_float2(0, 0);
+      if (rlane && b >= 0 && b < g.n[1]) {
+        const float4 *sb = ring + ((it - 1) % NST) * NW * 32 + lane;   // row b's f and sigma
+        CC sg0, sg1;
+        if (urow(b)) {
+          sg0 = sg1 = us;
+        } else {
+          const float4 v = sb[2 * 32];
+          sg0 = make_double2(v.x, v.y);
+          sg1 = make_double2(v.z, v.w);
+        }
+        const float4 fv = sb[32];
+        auto node = [&](CC cc, CC w_, CC e_, CC n_, CC s_, CC nw, CC ne, CC sw, CC se_, CC sgm, double fx, double fy) {
+          const CC sf = cadd<double>(cadd<double>(w_, e_), cadd<double>(n_, s_));
+          CC Lx = cscale<double>(cc, W::Lc);
+          Lx = cfmar<double>(Lx, W::Lf, sf);
+          if (W::Le != 0.0) Lx = cfmar<double>(Lx, W::Le, cadd<double>(cadd<double>(nw, ne), cadd<double>(sw, se_)));
+          Lx = cscale<double>(Lx, ih2);
+          CC Mx = cscale<double>(cc, W::Mc);
+          if (W::Mf != 0.0) Mx = cfmar<double>(Mx, W::Mf, sf);
+          sgm.y = fma(-alpha, sgm.x, sgm.y);
+          return csub<double>(make_double2(fx, fy), csub<double>(Lx, cmul<double>(sgm, Mx)));
+        };
+        if (in0) {
+          const CC o0 = node(b0, bw, b1, a0, c0, aw, a1, cw, c1, sg0, fv.x, fv.y);
+          r0 = make_float2((float)o0.x, (float)o0.y);
+        }
+        if (in1) {
+          const CC o1 = node(b1, b0, be, a1, c1, a0, ae, c0, ce, sg1, fv.z, fv.w);
+          r1 = make_float2((float)o1.x, (float)o1.y);
+        }
+      }
+      // x-pass of the restriction at coarse column X (fine 2X = x0): r at x0-2, x0-1 (left
+      // lane's pair), x0, x0+1 (own), x0+2 (right lane's first)
+      const float2 lm2 = make_float2(__shfl_up_sync(0xffffffffu, r0.x, 1), __shfl_up_sync(0xffffffffu, r0.y, 1));
+      const float2 lm1 = make_float2(__shfl_up_sync(0xffffffffu, r1.x, 1), __shfl_up_sync(0xffffffffu, r1.y, 1));
+      const float2 rp2 = make_float2(__shfl_down_sync(0xffffffffu, r0.x, 1), __shfl_down_sync(0xffffffffu, r0.y, 1));
+      CC hx = make_double2(0, 0);
+      hx = cfmar<double>(hx, w2, ccast<double, float>(lm2));
+      hx = cfmar<double>(hx, w1, ccast<double, float>(lm1));
+      hx = cfmar<double>(hx, w0, ccast<double, float>(r0));
+      hx = cfmar<double>(hx, w1, ccast<double, float>(r1));
+      hx = cfmar<double>(hx, w2, ccast<double, float>(rp2));
+      // y-pass: fine row b = 2 I0 + ky.  Even b: completes row I0 - 1 (ky = +2), continues
+      // I0 (ky = 0), opens I0 + 1 (ky = -2).  Odd b: ky = +1 for I0, -1 for I0 + 1.
+      if ((b & 1) == 0) {
+        P = cfmar<double>(P, w2, hx);
+        const int I = (b >> 1) - 1;
+        if (clane && I >= 0 && I < gc.n[1] && 2 * I >= y0 && 2 * I < y1) fc[gc.idx(X, I, 0)] = P;
+        Q = cfmar<double>(Q, w0, hx);
+        P = Q;
+        Q = cfmar<double>(make_double2(0, 0), w2, hx);
+      } else {
+        P = cfmar<double>(P, w1, hx);
+        Q = cfmar<double>(Q, w1, hx);
+      }
+    }
+    a0 = b0; a1 = b1; aw = bw; ae = be;
+    b0 = c0; b1 = c1; bw = cw; be = ce;
+  }
+}
+
 // Stored stencil of radius R: coef[k][j], k = (ox+R) + (2R+1)((oy+R) + (2R+1)(oz+R)),
 // multiplies x[j + o].  Coefficients towards out-of-domain nodes are zero.
 // TV = vector storage/arithmetic (fp64 on Galerkin levels), TK = coefficient storage.
@@ -416,6 +557,123 @@ __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *_
     const int64_t i = i0 + (int64_t)o * px;
     y[i] = f ? csub<T>(f[i], a0[o]) : a0[o];
     if (two) y[i + 1] = f ? csub<T>(f[i + 1], a1[o]) : a1[o];
+  }
+}
+
+// Level-l residual / apply of the stored radius-R stencil (2D, c64 path: fp32 coefficient
+// planes, fp64 level vectors) as a WARP-MARCHING kernel: lane l holds the column pair
+// (x0, x0 + 1), x0 = 60 s - 2 + 2 l (lanes 1..30 write, 0 and 31 supply neighbours), the
+// warp marches down SEG output rows; every input row is loaded once (32 bytes per lane
+// through a cp.async ring, PD rows ahead), its +-R column neighbours come from the
+// neighbour lanes by shuffles, and it is added at once to the 2R + 1 output rows it
+// reaches (rolling accumulators).  Each output accumulates its terms in the offset order
+// k = (oy + R)(2R + 1) + ox + R ascending -- the arithmetic of k_stored_op2d_pair.
+// Coefficients come from the uniform-box copy inside the box, else from the stored planes.
+constexpr int SM_STRIP = 60;
+template <int R, int SEG, int PD>
+__global__ void __launch_bounds__(128) k_stored_op2d_march(Geo g, const float2 *__restrict__ coef,
+                                                           const double2 *__restrict__ x,
+                                                           const double2 *__restrict__ f, double2 *__restrict__ y,
+                                                           UBox ub, UCoef<(2 * R + 1) * (2 * R + 1), double> uc) {
+  static_assert(R == 2 || R == 1, "radius 1 or 2");
+  using T = double;
+  constexpr int W = 2 * R + 1, NST = PD + 2;
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nstrips = (g.n[0] + SM_STRIP - 1) / SM_STRIP;
+  const int strip = wid % nstrips, seg = wid / nstrips;
+  const int y0 = seg * SEG;
+  if (y0 >= g.n[1]) return;
+  const int y1 = min(g.n[1], y0 + SEG);
+  const int x0 = strip * SM_STRIP - 2 + 2 * lane;
+  const bool out_lane = lane >= 1 && lane <= 30 && x0 < g.n[0];
+  const bool two = x0 + 1 < g.n[0];
+  const bool xload = x0 < g.n[0] + g.G;   // columns past the ghost layer are never used
+  // both nodes of the pair inside the box's columns (rows are checked per output row)
+  const bool xuni = x0 >= ub.lo[0] && (two ? x0 + 1 : x0) < ub.hi[0];
+  extern __shared__ __align__(16) unsigned char sm_smem[];
+  double2 *ring = reinterpret_cast<double2 *>(sm_smem) + (size_t)(threadIdx.x >> 5) * (NST * 2 * 32);
+  const int64_t px = g.px;
+  const int64_t ob0 = g.base + x0 + (int64_t)(y0 - R) * px;   // input row y0 - R, column x0
+  const int nin = y1 - y0 + 2 * R;                               // input rows y0-R .. y1-1+R
+  auto issue = [&](int it) {
+    if (it < nin) {
+      const int slot = it % NST;
+      const double2 *src = x + ob0 + (int64_t)it * px;
+      for (int h = 0; h < 2; ++h) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(ring + (slot * 2 + h) * 32 + lane);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(xload ? src + h : x),
+                     "r"(xload ? 16 : 0)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int k = 0; k < PD; ++k) issue(k);
+  auto shl = [](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
+  auto shr = [](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
+  // acc[q][n]: output row (input row - R + q) ... rolling: slot 0 = the oldest output row
+  double2 a0[W], a1[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) a0[q] = a1[q] = make_double2(0, 0);
+  for (int it = 0; it < nin; ++it) {
+    issue(it + PD);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(PD) : "memory");
+    const double2 *sl = ring + (it % NST) * 2 * 32 + lane;
+    const double2 c0 = sl[0], c1 = sl[32];
+    // window of the row: columns x0-2 .. x0+3
+    double2 xw[6];
+    xw[2] = c0;
+    xw[3] = c1;
+    xw[1] = make_double2(shl(c1.x), shl(c1.y));
+    xw[4] = make_double2(shr(c0.x), shr(c0.y));
+    if (R == 2) {
+      xw[0] = make_double2(shl(c0.x), shl(c0.y));
+      xw[5] = make_double2(shr(c1.x), shr(c1.y));
+    } else {
+      xw[0] = xw[5] = make_double2(0, 0);
+    }
+    const int yin = y0 - R + it;   // this input row
+    // add it to the outputs yo = yin - oy, oy = -R..R (accumulator q = R - oy ... newest last)
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const int oy = R - q;           // offset of the input row for the output in accumulator q
+      const int yo = yin - oy;
+      if (yo < y0 || yo >= y1 || !out_lane) continue;
+      const bool uni = xuni && yo >= ub.lo[1] && yo < ub.hi[1];
+      const int64_t io = ob0 + (int64_t)(yo - y0 + R) * px;
+#pragma unroll
+      for (int ox = -R; ox <= R; ++ox) {
+        const int k = (oy + R) * W + ox + R;
+        double2 k0, k1;
+        if (uni) {
+          k0 = k1 = uc.c[k];
+        } else {
+          const float4 cc = *reinterpret_cast<const float4 *>(coef + (int64_t)k * g.total + io);
+          k0 = mkc<T>(cc.x, cc.y);
+          k1 = mkc<T>(cc.z, cc.w);
+        }
+        a0[q] = cfma<T>(a0[q], k0, xw[ox + 2]);
+        a1[q] = cfma<T>(a1[q], k1, xw[ox + 3]);
+      }
+    }
+    // output row yin - R (accumulator 0) is complete
+    const int yo = yin - R;
+    if (yo >= y0 && yo < y1 && out_lane) {
+      const int64_t io = ob0 + (int64_t)(yo - y0 + R) * px;
+      if (f) {
+        const double2 f0 = f[io];
+        y[io] = csub<T>(f0, a0[0]);
+        if (two) y[io + 1] = csub<T>(f[io + 1], a1[0]);
+      } else {
+        y[io] = a0[0];
+        if (two) y[io + 1] = a1[0];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q + 1 < W; ++q) { a0[q] = a0[q + 1]; a1[q] = a1[q + 1]; }
+    a0[W - 1] = a1[W - 1] = make_double2(0, 0);
   }
 }
 

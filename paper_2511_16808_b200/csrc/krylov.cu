@@ -4,6 +4,7 @@
 #include "k_krylov.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <unordered_map>
@@ -78,6 +79,14 @@ int krylov_axpy(int nv, const cplx<TV> *V, int64_t vstride, const double2 *coef,
   return 0;
 }
 
+// c64 Arnoldi kernels can process two elements per thread and trip (loads of both first) up to
+// HMG_KRY_U2_MAX basis vectors; measured slower at N = 4096 (multi-AXPY 275 -> 289 ms per solve
+// with 10, 337 with 20), so the default is 0 (one element per trip)
+static int u2max() {
+  static const int v = std::getenv("HMG_KRY_U2_MAX") ? std::atoi(std::getenv("HMG_KRY_U2_MAX")) : 0;
+  return v;
+}
+
 // c64 Arnoldi: 16-byte (two complex) loads
 template <>
 int krylov_multidot<float, float>(int nv, bool self, const float2 *V, int64_t vstride, const float2 *w, int64_t len,
@@ -89,15 +98,15 @@ int krylov_multidot<float, float>(int nv, bool self, const float2 *V, int64_t vs
   const int64_t len2 = len / 2, vs2 = vstride / 2;
   if (self) {
     switch (nv) {
-#define C_(N) case N: { auto k = k_multidot_f4<N, true>; const int nb = wave_blocks(k, len2); \
-                        launch(k, dim3(nb), b, 0, s, V4, vs2, w4, len2, partial); return nb; }
+#define C_(N) case N: { auto k = N <= u2max() ? k_multidot_f4<N, true, 2> : k_multidot_f4<N, true, 1>; \
+                        const int nb = wave_blocks(k, len2); launch(k, dim3(nb), b, 0, s, V4, vs2, w4, len2, partial); return nb; }
       HMG_NV_CASES(C_)
 #undef C_
     }
   } else {
     switch (nv) {
-#define C_(N) case N: { auto k = k_multidot_f4<N, false>; const int nb = wave_blocks(k, len2); \
-                        launch(k, dim3(nb), b, 0, s, V4, vs2, w4, len2, partial); return nb; }
+#define C_(N) case N: { auto k = N <= u2max() ? k_multidot_f4<N, false, 2> : k_multidot_f4<N, false, 1>; \
+                        const int nb = wave_blocks(k, len2); launch(k, dim3(nb), b, 0, s, V4, vs2, w4, len2, partial); return nb; }
       HMG_NV_CASES(C_)
 #undef C_
     }
@@ -117,14 +126,16 @@ int krylov_axpy<float, float>(int nv, const float2 *V, int64_t vstride, const do
   const int64_t len2 = len / 2, vs2 = vstride / 2;
   if (partial_norm) {
     switch (nv) {
-#define C_(N) case N: { auto k = k_multi_axpy_f4<N, true>; const int nb = wave_blocks(k, len2); \
+#define C_(N) case N: { auto k = N <= u2max() ? k_multi_axpy_f4<N, true, 2> : k_multi_axpy_f4<N, true, 1>; \
+                        const int nb = wave_blocks(k, len2); \
                         launch(k, dim3(nb), b, 0, s, V4, vs2, coef, vscale, sgn, w4, len2, partial_norm); return nb; }
       HMG_NV_CASES(C_)
 #undef C_
     }
   } else {
     switch (nv) {
-#define C_(N) case N: { auto k = k_multi_axpy_f4<N, false>; const int nb = wave_blocks(k, len2); \
+#define C_(N) case N: { auto k = N <= u2max() ? k_multi_axpy_f4<N, false, 2> : k_multi_axpy_f4<N, false, 1>; \
+                        const int nb = wave_blocks(k, len2); \
                         launch(k, dim3(nb), b, 0, s, V4, vs2, coef, vscale, sgn, w4, len2, (double2 *)nullptr); return nb; }
       HMG_NV_CASES(C_)
 #undef C_

@@ -124,3 +124,75 @@ def test_vanka_blocked_bit_identical(monkeypatch, dim, vbz):
     ga.vcycle(q, za)
     gb.vcycle(q, zb)
     assert torch.equal(za, zb)
+
+
+@pytest.mark.parametrize("medium,n", [("homogeneous", 512), ("hetero", 520)])
+def test_stored_march_bit_identical(monkeypatch, medium, n):
+    """The warp-marching stored-stencil residual (k_stored_op2d_march, opt-in HMG_SMARCH=8, levels
+    with >= 256 rows) against the register-blocked gather (default): bit-identical level-1
+    residuals, V-cycles and FGMRES solves (c64; uniform box and heterogeneous medium)."""
+    import torch
+    from paper_2511_16808_b200 import hmg, media
+    p = media.config_problem(1, n=n) if medium == "homogeneous" else problem(2, (n, 264))
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=4, smoother="rb", damping=DAMPING[(2, "rb")], dtype="c64")
+    monkeypatch.setenv("HMG_SMARCH", "8")
+    ga = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.25)
+    monkeypatch.delenv("HMG_SMARCH")
+    gb = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.25)
+    N1 = ga.level_nodes(1)[0]
+    x = torch.from_numpy(media.random_complex(N1, 2)).to(torch.complex64).cuda()
+    f = torch.from_numpy(media.random_complex(N1, 3)).to(torch.complex64).cuda()
+    ra, rb = torch.empty_like(x), torch.empty_like(x)
+    ga.residual(f, x, ra, level=1, shifted=True)
+    gb.residual(f, x, rb, level=1, shifted=True)
+    assert torch.equal(ra, rb)
+    ga.apply_helmholtz(x, ra, level=1, shifted=True)
+    gb.apply_helmholtz(x, rb, level=1, shifted=True)
+    assert torch.equal(ra, rb)
+    q = torch.from_numpy(p.q.ravel()).to(torch.complex64).cuda()
+    za, zb = torch.zeros_like(q), torch.zeros_like(q)
+    ga.vcycle(q, za)
+    gb.vcycle(q, zb)
+    assert torch.equal(za, zb)
+    xa, xb = torch.zeros_like(q), torch.zeros_like(q)
+    r1 = ga.fgmres_solve(q, xa, restart=20, tol=1e-6, maxiter=600)
+    r2 = gb.fgmres_solve(q, xb, restart=20, tol=1e-6, maxiter=600)
+    assert r1.iterations == r2.iterations and torch.equal(xa, xb)
+
+
+@pytest.mark.parametrize("medium,cells,stencil", [
+    ("homogeneous", (256, 256), "compact4"),
+    ("hetero", (120, 68), "compact4"),
+    ("hetero", (8, 40), "compact4"),
+    ("hetero", (64, 32), "fd2"),
+])
+def test_residual_restrict_fused_bit_identical(monkeypatch, medium, cells, stencil):
+    """The fused fine residual + bicubic restriction (k_fine_resrestrict2d_march: residual
+    never written) against the residual kernel followed by k_restrict_pair (HMG_NO_RRFUSE=1):
+    bit-identical V-cycles and FGMRES solves on ragged grids (strip 56, segment 32)."""
+    import torch
+    from paper_2511_16808_b200 import hmg, media
+    p = media.config_problem(1, n=cells[0]) if medium == "homogeneous" else problem(2, cells)
+    opts = hmg.Options(dim=2, cells=p.cells, h=p.h, levels=3, smoother="rb", fine_stencil=stencil,
+                       damping=DAMPING[(2, "rb")], dtype="c64")
+    monkeypatch.delenv("HMG_NO_RRFUSE", raising=False)
+    ga = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.3)
+    monkeypatch.setenv("HMG_NO_RRFUSE", "1")
+    gb = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.3)
+    monkeypatch.delenv("HMG_NO_RRFUSE")
+    for seed in (1, 2):
+        f = torch.from_numpy(media.random_complex(p.n, seed)).to(torch.complex64).cuda()
+        za, zb = torch.zeros_like(f), torch.zeros_like(f)
+        ga.vcycle(f, za)
+        gb.vcycle(f, zb)
+        assert torch.equal(za, zb)
+        u = torch.from_numpy(media.random_complex(p.n, seed + 10)).to(torch.complex64).cuda()
+        ua, ub = u.clone(), u.clone()
+        ga.vcycle(f, ua, x_is_zero=False)
+        gb.vcycle(f, ub, x_is_zero=False)
+        assert torch.equal(ua, ub)
+    q = torch.from_numpy(p.q.ravel()).to(torch.complex64).cuda()
+    xa, xb = torch.zeros_like(q), torch.zeros_like(q)
+    r1 = ga.fgmres_solve(q, xa, restart=10, tol=1e-6, maxiter=400)
+    r2 = gb.fgmres_solve(q, xb, restart=10, tol=1e-6, maxiter=400)
+    assert r1.iterations == r2.iterations and torch.equal(xa, xb)
