@@ -34,6 +34,7 @@
 #include "k_vanka.cuh"
 #include "k_uniform.cuh"
 #include "k_stage3d.cuh"
+#include "k_tail.cuh"
 
 namespace hmg {
 
@@ -356,6 +357,10 @@ template <typename T> struct Solver : SolverBase {
   int smarch = 0;         // 2D c64 stored stencil: warp-marching kernel on large levels, segment height
                           // (HMG_SMARCH=8|16 at build; off by default: measured slower than the blocked gather)
   bool rrfuse = true;     // 2D c64 fine residual + restriction fused (HMG_NO_RRFUSE=1 at build)
+  // persistent coarse tail (k_tail.cuh): levels >= tail_l0 of a V(1,1) cycle in one launch
+  int tail_l0 = -1;
+  DBuf tail_lv, tail_uc, tail_bar;
+  int tail_grid = 0;
   DBuf rb_ia, rb_id;      // its sigma-only factors 1/a_j and 1/(a_c - e^2 sum 1/a_l), stored in T
   C usig{}, uia{}, uid{};  // level-0 uniform-box values of sig, rb_ia, rb_id
   D usigd{};
@@ -621,7 +626,115 @@ template <typename T> struct Solver : SolverBase {
     CK(cudaEventCreateWithFlags(&ev_dots, cudaEventDisableTiming));
     CK(cudaMallocHost((void **)&hpin, 4096 * sizeof(double)));
     find_uniform(s);
+    setup_tail(s);
     CK(cudaStreamSynchronize(s));
+  }
+
+  // ------------------------------------------------------ persistent coarse tail
+  // The levels below HMG_TAIL_NODES nodes of a one-rank V(1,1) cycle run as ONE persistent
+  // kernel (k_coarse_tail; HMG_TAIL_NODES=0 disables; default below).  Device table of
+  // TailLevel + the uniform-box copies in fp64 + a grid-barrier word pair, own per solver
+  // (per-stream clones build their own: concurrent launches must not share the barrier).
+  template <int DIM, int KIND> static void *tail_kernel() { return (void *)k_coarse_tail<T, DIM, KIND>; }
+  void *tail_fn() const {
+    const int d = opt.dim;
+    switch (opt.smoother) {
+      case HMG_VANKA_RB: return tail_kernel<2, PK_RB>();
+      case HMG_VANKA_ELEMENT: return d == 2 ? tail_kernel<2, PK_ELEMENT>() : tail_kernel<3, PK_ELEMENT>();
+      case HMG_JACOBI: return d == 2 ? tail_kernel<2, PK_JACOBI>() : tail_kernel<3, PK_JACOBI>();
+      case HMG_VANKA_PLUS: return d == 2 ? tail_kernel<2, PK_PLUS>() : tail_kernel<3, PK_PLUS>();
+    }
+    return nullptr;
+  }
+  void setup_tail(cudaStream_t s) {
+    tail_l0 = -1;
+    // default: 3D only (config 3: 3.50 -> 3.40 ms per iteration); in 2D the per-kernel graph is
+    // faster (N = 4096: levels >= 4 in one tail launch 177 us per cycle, the solve 1.505 -> 1.543 s)
+    const int64_t thr = std::getenv("HMG_TAIL_NODES") ? std::atoll(std::getenv("HMG_TAIL_NODES"))
+                                                      : (opt.dim == 3 ? 300000 : 0);
+    if (thr <= 0 || L < 3 || (comm && comm->size > 1) || opt.cycle != 0 || opt.nu1 != 1 || opt.nu2 != 1) return;
+    int l0 = -1;
+    for (int l = 1; l + 1 < L; ++l)
+      if (lev[l].geo.nodes() <= thr) { l0 = l; break; }
+    if (l0 < 0) return;
+    std::vector<TailLevel> tl(L);
+    std::vector<double2> uc;   // all uniform copies, offsets recorded per level
+    std::vector<size_t> oc(L, 0), ob(L, 0);
+    for (int l = l0; l < L; ++l) {
+      oc[l] = uc.size();
+      for (const C &c : lev[l].ucoef) uc.push_back(make_double2((double)c.x, (double)c.y));
+      ob[l] = uc.size();
+      for (const C &c : lev[l].ubop) uc.push_back(make_double2((double)c.x, (double)c.y));
+    }
+    tail_uc.alloc(std::max<size_t>(1, uc.size()) * sizeof(double2), s);
+    if (!uc.empty()) CK(cudaMemcpyAsync(tail_uc.p, uc.data(), uc.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+    for (int l = l0; l < L; ++l) {
+      TailLevel &t = tl[l];
+      const Level &Lv = lev[l];
+      t.geo = Lv.geo;
+      t.r = Lv.r;
+      t.rR = Lv.rR;
+      t.rP = Lv.rP;
+      t.w = damp(l);
+      t.coef = Lv.coef.p;
+      t.bop = Lv.bop.p;
+      t.ub = Lv.ub;
+      t.ucoef = tail_uc.template as<double2>() + oc[l];
+      t.ubop = tail_uc.template as<double2>() + ob[l];
+      t.u = Lv.u.template as<double2>();
+      t.f = Lv.f.template as<double2>();
+      t.r_ = Lv.r_.template as<double2>();
+    }
+    tail_lv.alloc(L * sizeof(TailLevel), s);
+    CK(cudaMemcpyAsync(tail_lv.p, tl.data(), L * sizeof(TailLevel), cudaMemcpyHostToDevice, s));
+    tail_bar.alloc(2 * sizeof(unsigned), s);
+    int per_sm = 0, dev = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_fn(), 256, 0));
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    tail_grid = std::max(1, std::min(per_sm, 2)) * sms;   // co-resident (cooperative launch, launch_tail)
+    CK(cudaStreamSynchronize(s));
+    tail_l0 = l0;
+  }
+  void launch_tail(cudaStream_t s) {
+    const TailLevel *tl = tail_lv.template as<TailLevel>();
+    const D *ai = ainv.template as<D>();
+    unsigned *bar = tail_bar.template as<unsigned>();
+    tag("coarse_tail", tail_l0, 0.0);
+    // cooperative launch: the driver guarantees every block is resident at once (the software
+    // grid barrier needs it, also when other streams run tails concurrently); capturable
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tail_grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    auto go = [&](auto kern) {
+      const int pi = prof_before(s);
+      CK(cudaLaunchKernelEx(&cfg, kern, tl, tail_l0, L, ai, bar));
+      count_launch();
+      prof_after(s, pi);
+    };
+    const int d = opt.dim;
+    switch (opt.smoother) {
+      case HMG_VANKA_RB: go(k_coarse_tail<T, 2, PK_RB>); break;
+      case HMG_VANKA_ELEMENT:
+        if (d == 2) go(k_coarse_tail<T, 2, PK_ELEMENT>);
+        else go(k_coarse_tail<T, 3, PK_ELEMENT>);
+        break;
+      case HMG_JACOBI:
+        if (d == 2) go(k_coarse_tail<T, 2, PK_JACOBI>);
+        else go(k_coarse_tail<T, 3, PK_JACOBI>);
+        break;
+      case HMG_VANKA_PLUS:
+        if (d == 2) go(k_coarse_tail<T, 2, PK_PLUS>);
+        else go(k_coarse_tail<T, 3, PK_PLUS>);
+        break;
+    }
   }
 
   // ------------------------------------------------------ uniform-box compression
@@ -1516,6 +1629,10 @@ template <typename T> struct Solver : SolverBase {
       coarse_(f, u, s);
       return;
     }
+    if (l == tail_l0 && zero && nrb == 1 && f == lev[l].f.p && u == lev[l].u.p) {   // levels >= l: one launch
+      launch_tail(s);
+      return;
+    }
     Level &Lv = lev[l];
     for (int k = 0; k < opt.nu1; ++k) {                        // step 1: pre-smoothing
       if (k == 0 && zero) smooth(l, f, nullptr, u, 1, s);      //   zero guess: r = f, u written only
@@ -1833,6 +1950,7 @@ template <typename T> struct Solver : SolverBase {
     for (auto &kv : fgraphs) cudaGraphExecDestroy(kv.second.first);
     fgraphs.clear();
     nrb_cap = nr;
+    setup_tail(s);   // its level table points at the reallocated vectors
   }
 
   // Start (or restart) the Arnoldi process of a bound state: r = q - H x in fp64,
@@ -2136,6 +2254,7 @@ template <typename T> struct Solver : SolverBase {
     CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreateWithFlags(&c->ev_dots, cudaEventDisableTiming));
     CK(cudaMallocHost((void **)&c->hpin, 4096 * sizeof(double)));
+    c->setup_tail(s);
     CK(cudaStreamSynchronize(s));
     return std::unique_ptr<SolverBase>(c.release());
   }
