@@ -54,6 +54,7 @@ struct LocalGroup {
 };
 
 __global__ void k_sum_stage(const double *__restrict__ stage, int nranks, int n, double *__restrict__ out) {
+  HMG_PDL_PROLOGUE();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double a = 0;

@@ -145,6 +145,18 @@ inline NodeLaunch node_launch(const Geo &g) {
 // launch accounting (hmg_launch_count) -- incremented by every launch
 void count_launch();
 
+// Programmatic dependent launch (runtime.cuh launch()): every kernel of the library
+// starts with this prologue.  griddepcontrol.wait blocks until the grids this one
+// depends on have completed and their memory is visible, so nothing is read early;
+// launch_dependents lets the NEXT kernel's blocks be scheduled once every block of
+// this grid has started, hiding its launch latency behind this grid's tail.  Both are
+// no-ops for a normal launch.
+#define HMG_PDL_PROLOGUE()                                   \
+  do {                                                       \
+    asm volatile("griddepcontrol.wait;" ::: "memory");       \
+    asm volatile("griddepcontrol.launch_dependents;" :::);   \
+  } while (0)
+
 }  // namespace hmg
 
 #define HMG_NODE_IDX(g, X_, Y_, Z_)                           \

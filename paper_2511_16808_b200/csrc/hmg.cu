@@ -40,6 +40,10 @@ namespace hmg {
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool pdl_enabled() {
+  static const bool on = std::getenv("HMG_NO_PDL") == nullptr && std::getenv("HMG_PDL") != nullptr;
+  return on;
+}
 long long launch_count_now() { return g_launches.load(); }
 void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
@@ -184,6 +188,7 @@ static int patch_size(int dim, int kind) {
 }
 
 __global__ void k_identity(int N, double2 *__restrict__ A) {
+  HMG_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < (int64_t)N * N) A[i] = make_double2((i / N) == (i % N) ? 1.0 : 0.0, 0.0);
 }
@@ -193,6 +198,7 @@ __global__ void k_identity(int N, double2 *__restrict__ A) {
 template <typename T, int NR = 1>
 __global__ void k_coarse_gemv(Geo g, const double2 *__restrict__ Ainv, const cplx<T> *__restrict__ r,
                               cplx<T> *__restrict__ e, int64_t bs = 0) {
+  HMG_PDL_PROLOGUE();
   const int N = (int)g.nodes();
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;

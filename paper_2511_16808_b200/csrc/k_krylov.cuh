@@ -27,6 +27,7 @@ template <typename TV, typename TW, int NV, bool SELF>
 __global__ void __launch_bounds__(KRY_THREADS) k_multidot(const cplx<TV> *__restrict__ V, int64_t vstride,
                                                           const cplx<TW> *__restrict__ w, int64_t len,
                                                           double2 *__restrict__ partial) {
+  HMG_PDL_PROLOGUE();
   constexpr int NA = NV + (SELF ? 1 : 0);
   constexpr int U = NV <= 2 ? 4 : NV <= 5 ? 2 : 1;   // elements per thread per pass: >= ~8 loads in flight
   double ar[NA], ai[NA];
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multidot(const cplx<TV> *__rest
 
 // out[i] = sum_b partial[i * nblk + b]  (one warp per i, fixed order)
 static __global__ void k_reduce_partials(const double2 *__restrict__ partial, int nblk, int nv, double2 *__restrict__ out) {
+  HMG_PDL_PROLOGUE();
   const int i = blockIdx.x;
   if (i >= nv) return;
   double a = 0, b = 0;
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy(const cplx<TV> *__re
                                                             const double2 *__restrict__ coef, const double *vscale,
                                                             double sgn, cplx<TW> *__restrict__ w, int64_t len,
                                                             double2 *__restrict__ partial) {
+  HMG_PDL_PROLOGUE();
   __shared__ double2 sc[NV];
   if (threadIdx.x < NV) {
     const double f = sgn * (vscale ? vscale[threadIdx.x] : 1.0);
@@ -154,6 +157,7 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy(const cplx<TV> *__re
 template <typename TI, typename TO = TI>
 __global__ void __launch_bounds__(KRY_THREADS) k_scale(const cplx<TI> *__restrict__ w, cplx<TO> *__restrict__ v,
                                                        double s, int64_t len) {
+  HMG_PDL_PROLOGUE();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += stride) {
     const cplx<TI> a = w[e];
@@ -168,6 +172,7 @@ template <int NV, bool SELF, int U = 1>
 __global__ void __launch_bounds__(KRY_THREADS) k_multidot_f4(const float4 *__restrict__ V, int64_t vstride2,
                                                              const float4 *__restrict__ w, int64_t len2,
                                                              double2 *__restrict__ partial) {
+  HMG_PDL_PROLOGUE();
   constexpr int NA = NV + (SELF ? 1 : 0);
   double ar[NA], ai[NA];
 #pragma unroll
@@ -229,6 +234,7 @@ __global__ void __launch_bounds__(KRY_THREADS) k_multi_axpy_f4(const float4 *__r
                                                                const double2 *__restrict__ coef, const double *vscale,
                                                                double sgn, float4 *__restrict__ w, int64_t len2,
                                                                double2 *__restrict__ partial) {
+  HMG_PDL_PROLOGUE();
   __shared__ double2 sc[NV];
   if (threadIdx.x < NV) {
     const double f = sgn * (vscale ? vscale[threadIdx.x] : 1.0);

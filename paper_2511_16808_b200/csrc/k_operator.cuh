@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(256) k_fine_op(Geo g, const cplx<TS> *__restri
                                                  const cplx<T> *__restrict__ x,
                                                  const cplx<T> *__restrict__ f, cplx<T> *__restrict__ y,
                                                  UBox ub, cplx<TC> us) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t i = g.idx(ix, iy, iz);
   y[i] = fine_op_node<T, DIM, KIND, TC, TS>(g, sig, alpha, ih2, x, f, i, ub.in(ix, iy, iz), us);
@@ -101,6 +102,7 @@ template <int KIND, typename TC, typename TSG>
 __global__ void __launch_bounds__(256) k_fine_op2d_pair(Geo g, const cplx<TSG> *__restrict__ sig, TC alpha, TC ih2,
                                                         const float2 *__restrict__ x, const float2 *__restrict__ f,
                                                         float2 *__restrict__ y, UBox ub, cplx<TC> us) {
+  HMG_PDL_PROLOGUE();
   using W = FineW<2, KIND>;
   using CC = cplx<TC>;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(128) k_fine_op2d_march(Geo g, const cplx<TSG> 
                                                          double ih2, const float2 *__restrict__ x,
                                                          const float2 *__restrict__ f, float2 *__restrict__ y, UBox ub,
                                                          double2 us) {
+  HMG_PDL_PROLOGUE();
   using W = FineW<2, KIND>;
   using CC = double2;
   const int lane = threadIdx.x & 31;
@@ -290,6 +293,7 @@ __global__ void __launch_bounds__(128) k_fine_resrestrict2d_march(Geo g, Geo gc,
                                                                   const float2 *__restrict__ x,
                                                                   const float2 *__restrict__ f,
                                                                   double2 *__restrict__ fc, UBox ub, double2 us) {
+  HMG_PDL_PROLOGUE();
   using W = FineW<2, KIND>;
   using CC = double2;
   static_assert(SEG % 2 == 0, "segments start on even rows");
@@ -424,6 +428,7 @@ __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__rest
                                                    const cplx<TV> *__restrict__ x,
                                                    const cplx<TV> *__restrict__ f, cplx<TV> *__restrict__ y,
                                                    int64_t bs, UBox ub, UCoef<kplanes<DIM, R>(), TV> uc) {
+  HMG_PDL_PROLOGUE();
   // NR right-hand sides at a stride of bs elements: each coefficient is read once
   // and applied to all of them (multi-RHS batches; same per-RHS arithmetic order).
   // BZ consecutive nodes along the slowest axis per thread (register blocking: each
@@ -499,6 +504,7 @@ __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *_
                                                           const double2 *__restrict__ x,
                                                           const double2 *__restrict__ f, double2 *__restrict__ y,
                                                           UBox ub, UCoef<(2 * R + 1) * (2 * R + 1), double> uc) {
+  HMG_PDL_PROLOGUE();
   using T = double;
   constexpr int W = 2 * R + 1;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -575,6 +581,7 @@ __global__ void __launch_bounds__(128) k_stored_op2d_march(Geo g, const float2 *
                                                            const double2 *__restrict__ x,
                                                            const double2 *__restrict__ f, double2 *__restrict__ y,
                                                            UBox ub, UCoef<(2 * R + 1) * (2 * R + 1), double> uc) {
+  HMG_PDL_PROLOGUE();
   static_assert(R == 2 || R == 1, "radius 1 or 2");
   using T = double;
   constexpr int W = 2 * R + 1, NST = PD + 2;

@@ -11,11 +11,13 @@ namespace hmg {
 // unpadded x-fastest (N) <-> padded box
 template <typename A>
 __global__ void k_pack(Geo g, const A *__restrict__ src, A *__restrict__ dst) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   dst[g.idx(ix, iy, iz)] = src[((int64_t)iz * g.n[1] + iy) * g.n[0] + ix];
 }
 template <typename A>
 __global__ void k_unpack(Geo g, const A *__restrict__ src, A *__restrict__ dst) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   dst[((int64_t)iz * g.n[1] + iy) * g.n[0] + ix] = src[g.idx(ix, iy, iz)];
 }
@@ -24,6 +26,7 @@ __global__ void k_unpack(Geo g, const A *__restrict__ src, A *__restrict__ dst) 
 template <typename TI, typename TO>
 __global__ void k_pack_cvt(Geo g, const cplx<TI> *__restrict__ src, int src_padded, cplx<TO> *__restrict__ dst,
                            int dst_padded) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t c = ((int64_t)iz * g.n[1] + iy) * g.n[0] + ix;
   const int64_t p = g.idx(ix, iy, iz);
@@ -36,6 +39,7 @@ template <typename T>
 __global__ void k_sigma(Geo g, const double *__restrict__ kappa, const double *__restrict__ gamma, double omega,
                         double *__restrict__ w2k2, double *__restrict__ gq, cplx<T> *__restrict__ sig,
                         double2 *__restrict__ sigd) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t s = ((int64_t)iz * g.n[1] + iy) * g.n[0] + ix;
   const int64_t i = g.idx(ix, iy, iz);
@@ -60,6 +64,7 @@ __host__ __device__ __forceinline__ int kidx(int ox, int oy, int oz, int r, int 
 template <int DIM, int KIND>
 __global__ void k_materialize(Geo g, const double *__restrict__ w2k2, const double *__restrict__ gq, double alpha,
                               double ih2, double2 *__restrict__ coef) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   using W = FineW<DIM, KIND>;
   const int64_t i = g.idx(ix, iy, iz);
@@ -94,6 +99,7 @@ __host__ __device__ __forceinline__ int floordiv2(int a) { return a >= 0 ? a / 2
 template <int DIM, int RC>
 __global__ void k_galerkin(Geo gf, Geo gc, const double2 *__restrict__ cf, int rf, TransferW tw,
                            double2 *__restrict__ cc) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(gc, Xl, Yl, Zl);
   const int X = Xl + gc.o[0], Y = Yl + gc.o[1], Z = Zl + gc.o[2];   // global coarse node
   auto finside = [&](int x, int y, int z) {   // global fine node in the domain
@@ -150,6 +156,7 @@ __global__ void k_galerkin(Geo gf, Geo gc, const double2 *__restrict__ cf, int r
 // a7 (REDISCRETIZE): full-weighting average of a per-node field, normalised
 // by the in-domain weight sum (truncated lin R, reading A13).
 static __global__ void k_fw_average(Geo gf, Geo gc, const double *__restrict__ ff, double *__restrict__ fc) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(gc, Xl, Yl, Zl);
   const int X = Xl + gc.o[0], Y = Yl + gc.o[1], Z = Zl + gc.o[2];   // global (windows: Geo::o)
   const double w1[3] = {0.25, 0.5, 0.25};
@@ -170,6 +177,7 @@ static __global__ void k_fw_average(Geo gf, Geo gc, const double *__restrict__ f
 // cast a stored stencil (double) to the working precision
 template <typename T>
 __global__ void k_cast(const double2 *__restrict__ src, cplx<T> *__restrict__ dst, int64_t n) {
+  HMG_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = mkc<T>((T)src[i].x, (T)src[i].y);
 }
@@ -177,6 +185,7 @@ __global__ void k_cast(const double2 *__restrict__ src, cplx<T> *__restrict__ ds
 // stored stencil (T, padded) -> compact double [K][N] for hmg_copy_stencil
 template <typename T>
 __global__ void k_compact_stencil(Geo g, int K, const cplx<T> *__restrict__ src, double2 *__restrict__ dst) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t N = g.nodes();
   const int64_t s = ((int64_t)iz * g.n[1] + iy) * g.n[0] + ix;
@@ -230,6 +239,7 @@ __device__ bool small_inverse(double2 (&A)[K][K], double2 (&X)[K][K], int m) {
 template <typename T, int DIM, int KIND>
 __global__ void k_patch_inverse(Geo g, const double2 *__restrict__ coef, int r, cplx<T> *__restrict__ hinv,
                                 unsigned long long *__restrict__ err) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   using P = Patch<DIM, KIND>;
   constexpr int K = P::K;
@@ -269,6 +279,7 @@ __global__ void k_patch_inverse(Geo g, const double2 *__restrict__ coef, int r, 
 // (Eq. 3.8; non-anchor positions hold zero inverses).  fp64 sums, stored in T.
 template <typename T, int DIM, int KIND>
 __global__ void k_vanka_assemble(Geo g, const double2 *__restrict__ hinv, cplx<T> *__restrict__ B) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   using P = Patch<DIM, KIND>;
   using S = BStencil<DIM, KIND>;
@@ -297,6 +308,7 @@ __global__ void k_vanka_assemble(Geo g, const double2 *__restrict__ hinv, cplx<T
 
 // a8: dense coarsest matrix (row-major, compact x-fastest indices)
 static __global__ void k_dense_assemble(Geo g, const double2 *__restrict__ coef, int r, double2 *__restrict__ A) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t N = g.nodes();
   const int64_t row = ((int64_t)iz * g.n[1] + iy) * g.n[0] + ix;
@@ -315,6 +327,7 @@ static __global__ void k_dense_assemble(Geo g, const double2 *__restrict__ coef,
 // rows, scale the pivot row, save the elimination factors fcol[i] = A[i][k].
 static __global__ void k_gj_pivot(int N, int k, double2 *__restrict__ A, double2 *__restrict__ Ai,
                            double2 *__restrict__ fcol, int *__restrict__ err) {
+  HMG_PDL_PROLOGUE();
   __shared__ double sv[1024];
   __shared__ int si[1024];
   const int t = threadIdx.x;
@@ -356,6 +369,7 @@ static __global__ void k_gj_pivot(int N, int k, double2 *__restrict__ A, double2
 // Gauss-Jordan step k, part 2: eliminate column k from every other row.
 static __global__ void k_gj_eliminate(int N, int k, double2 *__restrict__ A, double2 *__restrict__ Ai,
                                const double2 *__restrict__ fcol) {
+  HMG_PDL_PROLOGUE();
   const int i = blockIdx.y;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == k || b >= N) return;

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(S3_THREADS) k_fine_op3d_z(Geo g, const __grid_
                                                             const __grid_constant__ CUtensorMap mf, int has_f,
                                                             TC alpha, TC ih2, cplx<T> *__restrict__ y, UBox ub,
                                                             cplx<TC> us) {
+  HMG_PDL_PROLOGUE();
   using W = FineW<3, KIND>;
   using E = cplx<T>;
   using CC = cplx<TC>;
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(S3_THREADS) k_vanka27_z(Geo g, const __grid_co
                                                           const cplx<TK> *__restrict__ B, const cplx<TV> *u,
                                                           cplx<TV> *u_out, TV w, int zero, UBox ub,
                                                           UCoef<27, TV> uc) {
+  HMG_PDL_PROLOGUE();
   using E = cplx<TV>;
   extern __shared__ __align__(128) unsigned char s3_smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(s3_smem), *empty = full + NS;

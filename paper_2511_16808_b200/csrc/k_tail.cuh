@@ -196,6 +196,7 @@ __device__ void tail_stored_pass(const TailLevel &L, const double2 *x, const dou
 template <typename TK, int DIM, int KIND>
 __global__ void __launch_bounds__(256) k_coarse_tail(const TailLevel *__restrict__ lv, int l0, int L,
                                                      const double2 *__restrict__ ainv, unsigned *bar) {
+  HMG_PDL_PROLOGUE();
   const unsigned nb = gridDim.x;
   for (int l = l0; l < L - 1; ++l) {
     const TailLevel &A = lv[l], &B = lv[l + 1];

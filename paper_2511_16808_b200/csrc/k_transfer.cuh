@@ -26,6 +26,7 @@ template <> struct RW<2> {
 template <typename TI, typename TO, int DIM, int RR>
 __global__ void __launch_bounds__(256) k_restrict(Geo gf, Geo gc, const cplx<TI> *__restrict__ r,
                                                   cplx<TO> *__restrict__ fc) {
+  HMG_PDL_PROLOGUE();
   using T = double;
   HMG_NODE_IDX(gc, X, Y, Z);
   const int64_t ic = gc.idx(X, Y, Z);
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(256) k_restrict(Geo gf, Geo gc, const cplx<TI>
 template <int DIM>
 __global__ void __launch_bounds__(256) k_restrict_pair(Geo gf, Geo gc, const float2 *__restrict__ r,
                                                        double2 *__restrict__ fc) {
+  HMG_PDL_PROLOGUE();
   using T = double;
   HMG_NODE_IDX(gc, X, Y, Z);
   const int64_t ic = gc.idx(X, Y, Z);
@@ -91,6 +93,7 @@ template <typename TE, typename TU, int DIM, int PR>
 __global__ void __launch_bounds__(256) k_prolong_block(Geo gf, Geo gc, int cx0, int cy0, int cz0, int ncx, int ncy,
                                                        int ncz, const cplx<TE> *__restrict__ e, const cplx<TU> *u,
                                                        cplx<TU> *u_out) {
+  HMG_PDL_PROLOGUE();
   using T = double;
   const int X = cx0 + (int)(blockIdx.x * blockDim.x + threadIdx.x);   // GLOBAL coarse coordinates
   const int Y = cy0 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
@@ -190,6 +193,7 @@ template <typename TSG, int KIND, int RR, int PR, int TX, int TY, typename TC = 
 __global__ void __launch_bounds__(256) k_galerkin1_mf(Geo gf, Geo gc, const cplx<TSG> *__restrict__ sig, double alpha,
                                                       double ih2, const double2 *__restrict__ u,
                                                       const double2 *__restrict__ f, double2 *__restrict__ y) {
+  HMG_PDL_PROLOGUE();
   using T = TC;
   using V = cplx<TC>;
   using W = FineW<2, KIND>;

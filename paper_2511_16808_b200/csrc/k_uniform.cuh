@@ -49,6 +49,7 @@ template <int K, typename TK> struct UCoef {
 template <typename E>
 __global__ void k_uniform_flags(Geo g, const E *__restrict__ planes, int nplanes, int64_t ref,
                                 unsigned char *__restrict__ flag) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   const int64_t j = g.idx(ix, iy, iz);
   const int64_t f = ((int64_t)iz * g.n[1] + iy) * g.n[0] + ix;

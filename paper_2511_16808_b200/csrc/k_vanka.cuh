@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(256) k_vanka_stencil(Geo g, const cplx<TK> *__
                                                        const cplx<T> *__restrict__ r, const cplx<T> *u,
                                                        cplx<T> *u_out, T w, int zero, int64_t bs, UBox ub,
                                                        UCoef<BStencil<DIM, KIND>::NB, T> uc) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   using S = BStencil<DIM, KIND>;
   const int64_t j = g.idx(ix, iy, iz);
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(256) k_vanka_stencil_blk(Geo g, const cplx<TK>
                                                            const cplx<T> *__restrict__ r, const cplx<T> *u,
                                                            cplx<T> *u_out, T w, int zero, UBox ub,
                                                            UCoef<BStencil<DIM, KIND>::NB, T> uc) {
+  HMG_PDL_PROLOGUE();
   using S = BStencil<DIM, KIND>;
   const int ix = blockIdx.x * blockDim.x + threadIdx.x;
   const int iyt = blockIdx.y * blockDim.y + threadIdx.y;
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(256) k_vanka_stencil_blk(Geo g, const cplx<TK>
 template <typename TS>
 __global__ void k_rb_factors(Geo g, const double2 *__restrict__ sigd, double alpha, double ih2, double Lc, double Mc,
                              double e, cplx<TS> *__restrict__ ia, cplx<TS> *__restrict__ id) {
+  HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   auto diag = [&](int x, int y) {
     double2 s = sigd[g.idx(x, y, 0)];
@@ -306,6 +309,7 @@ __global__ void __launch_bounds__(256, MINB) k_rb2d_march(Geo g, const cplx<TS> 
                                                     double alpha_d, double ih2_d, const cplx<TS> *__restrict__ f,
                                                     const cplx<TS> *__restrict__ u, cplx<TS> *__restrict__ u_out,
                                                     double w_d, UBox ub, cplx<TS> usg, cplx<TS> uia, cplx<TS> uid) {
+  HMG_PDL_PROLOGUE();
   using W = FineW<2, KIND>;
   using D = TC;
   const D alpha = (D)alpha_d, ih2 = (D)ih2_d, w = (D)w_d;
@@ -481,6 +485,7 @@ __global__ void __launch_bounds__(128, MINB) k_rb2d_march2(Geo g, const float2 *
                                                            double ih2_d, const float2 *__restrict__ f,
                                                            const float2 *__restrict__ u, float2 *__restrict__ u_out,
                                                            double w_d, UBox ub, float2 usg, float2 uia, float2 uid) {
+  HMG_PDL_PROLOGUE();
   using W = FineW<2, KIND>;
   using D = double;
   using CD = double2;

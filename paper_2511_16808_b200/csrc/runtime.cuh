@@ -35,11 +35,28 @@ void add_launches(long long n);
 int prof_before(cudaStream_t s);
 void prof_after(cudaStream_t s, int idx);
 
+// programmatic dependent launch on (non-legacy) streams (HMG_NO_PDL=1: plain launches)
+bool pdl_enabled();
+
 template <typename... KArgs, typename... Args>
 inline void launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args... args) {
   if (g.x == 0 || g.y == 0 || g.z == 0) return;
   const int pi = prof_before(s);
-  k<<<g, b, smem, s>>>(static_cast<KArgs>(args)...);
+  if (s != nullptr && pdl_enabled()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+  } else {
+    k<<<g, b, smem, s>>>(static_cast<KArgs>(args)...);
+  }
   count_launch();
   CK(cudaGetLastError());
   prof_after(s, pi);
