@@ -363,6 +363,7 @@ template <typename T> struct Solver : SolverBase {
   int smarch = 0;         // 2D c64 stored stencil: warp-marching kernel on large levels, segment height
                           // (HMG_SMARCH=8|16 at build; off by default: measured slower than the blocked gather)
   bool rrfuse = true;     // 2D c64 fine residual + restriction fused (HMG_NO_RRFUSE=1 at build)
+  bool zblock3 = true;    // 3D transfers with 4 coarse planes per thread (HMG_NO_ZBLOCK3=1 at build)
   // persistent coarse tail (k_tail.cuh): levels >= tail_l0 of a V(1,1) cycle in one launch
   int tail_l0 = -1;
   DBuf tail_lv, tail_uc, tail_bar;
@@ -422,6 +423,7 @@ template <typename T> struct Solver : SolverBase {
     rbfast = std::getenv("HMG_NO_RB_FAST") == nullptr;
     smarch = std::getenv("HMG_SMARCH") ? std::atoi(std::getenv("HMG_SMARCH")) : 0;
     rrfuse = std::getenv("HMG_NO_RRFUSE") == nullptr;
+    zblock3 = std::getenv("HMG_NO_ZBLOCK3") == nullptr;
     // measured: BZ = 2 helps the 3D element operator (config 3 level 0: 53 -> 50 ms per solve)
     // and hurts the 2D RB one (level 1 at N = 4096: 103 -> 117 ms)
     vanka_bz = std::getenv("HMG_VANKA_BZ") ? std::atoi(std::getenv("HMG_VANKA_BZ")) : (opt.dim == 3 ? 2 : 1);
@@ -1329,7 +1331,11 @@ template <typename T> struct Solver : SolverBase {
     if (l == 0 && F.rR == 2 && std::is_same<T, float>::value && (G % 2) == 0 && (F.geo.base % 2) == 0 && !nopr) {
       const float2 *r2 = reinterpret_cast<const float2 *>(r);   // c64 fine level: 16-byte pair loads
       if (opt.dim == 2) launch(k_restrict_pair<2>, nl.grid, nl.block, 0, s, F.geo, gc, r2, fc);
-      else launch(k_restrict_pair<3>, nl.grid, nl.block, 0, s, F.geo, gc, r2, fc);
+      else if (!F.dist && !Cc.gather_in && zblock3) {   // one rank: 4 coarse planes per thread
+        dim3 g4 = nl.grid;
+        g4.z = (gc.n[2] + 3) / 4;
+        launch(k_restrict_pair3_z<4>, g4, nl.block, 0, s, F.geo, gc, r2, fc);
+      } else launch(k_restrict_pair<3>, nl.grid, nl.block, 0, s, F.geo, gc, r2, fc);
     } else if (opt.dim == 2) {
       if (F.rR == 1) launch(k_restrict<BI, double, 2, 1>, nl.grid, nl.block, 0, s, F.geo, gc, r, fc);
       else launch(k_restrict<BI, double, 2, 2>, nl.grid, nl.block, 0, s, F.geo, gc, r, fc);
@@ -1366,6 +1372,12 @@ template <typename T> struct Solver : SolverBase {
       nc[a] = (fhi - 1) / 2 - c0[a] + 1;
     }
     const dim3 block(32, 8), grid((nc[0] + 31) / 32, (nc[1] + 7) / 8, opt.dim == 3 ? nc[2] : 1);
+    if (opt.dim == 3 && !F.dist && !Cc.dist && zblock3 && c0[2] == 0 && nc[2] == Cc.geo.n[2]) {
+      const dim3 g4((nc[0] + 31) / 32, (nc[1] + 7) / 8, (nc[2] + 3) / 4);   // one rank: 4 coarse planes per thread
+      if (F.rP == 1) launch(k_prolong3_z<BU, 1, 4>, g4, block, 0, s, F.geo, Cc.geo, e, u, uo);
+      else launch(k_prolong3_z<BU, 2, 4>, g4, block, 0, s, F.geo, Cc.geo, e, u, uo);
+      return;
+    }
     if (opt.dim == 2) {
       if (F.rP == 1) launch(k_prolong_block<double, BU, 2, 1>, grid, block, 0, s, F.geo, Cc.geo, c0[0], c0[1], c0[2], nc[0], nc[1], nc[2], e, u, uo);
       else launch(k_prolong_block<double, BU, 2, 2>, grid, block, 0, s, F.geo, Cc.geo, c0[0], c0[1], c0[2], nc[0], nc[1], nc[2], e, u, uo);
@@ -2232,6 +2244,7 @@ template <typename T> struct Solver : SolverBase {
     c->vanka_bz = vanka_bz;
     c->smarch = smarch;
     c->rrfuse = rrfuse;
+    c->zblock3 = zblock3;
     c->usig = usig; c->uia = uia; c->uid = uid; c->usigd = usigd;
     c->sig = DBuf::view(sig);
     c->sigd = DBuf::view(sigd);

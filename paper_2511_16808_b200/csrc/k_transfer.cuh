@@ -85,6 +85,118 @@ __global__ void __launch_bounds__(256) k_restrict_pair(Geo gf, Geo gc, const flo
   fc[ic] = acc;
 }
 
+// 3D c64 fine-level restriction with BZ coarse planes per thread: the in-plane (x, y)
+// restricted value accy(p) of a fine plane p does not depend on the coarse plane it feeds,
+// so each fine plane is loaded and reduced ONCE per thread and added, with the z weight,
+// to every coarse output it reaches (fine planes 2Z-2 .. 2Z+2 of output Z, in increasing
+// order = kz ascending): the arithmetic of k_restrict_pair<3>, 2BZ + 3 fine planes for BZ
+// outputs instead of 5 BZ.  One rank (no offsets).
+template <int BZ>
+__global__ void __launch_bounds__(256) k_restrict_pair3_z(Geo gf, Geo gc, const float2 *__restrict__ r,
+                                                          double2 *__restrict__ fc) {
+  HMG_PDL_PROLOGUE();
+  using T = double;
+  const int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int Z0 = blockIdx.z * BZ;
+  if (X >= gc.n[0] || Y >= gc.n[1] || Z0 >= gc.n[2]) return;
+  const int zl = min(BZ, gc.n[2] - Z0);   // outputs of this thread
+  double2 acc[BZ];
+#pragma unroll
+  for (int o = 0; o < BZ; ++o) acc[o] = make_double2(0, 0);
+  const int64_t jf0 = gf.idx(2 * X, 2 * Y, 2 * Z0);
+#pragma unroll
+  for (int q = -2; q <= 2 * BZ; ++q) {   // fine plane 2 Z0 + q
+    if (q > 2 * (zl - 1) + 2) break;
+    double2 accy = make_double2(0, 0);
+#pragma unroll
+    for (int ky = -2; ky <= 2; ++ky) {
+      const float4 *row = reinterpret_cast<const float4 *>(r + jf0 + gf.delta(-2, ky, q));
+      const float4 p0 = row[0], p1 = row[1], p2 = row[2];
+      const float2 v[5] = {make_float2(p0.x, p0.y), make_float2(p0.z, p0.w), make_float2(p1.x, p1.y),
+                           make_float2(p1.z, p1.w), make_float2(p2.x, p2.y)};
+      double2 accx = make_double2(0, 0);
+#pragma unroll
+      for (int kx = -2; kx <= 2; ++kx) accx = cfmar<T>(accx, RW<2>::w(kx), ccast<T, float>(v[kx + 2]));
+      accy = cfmar<T>(accy, RW<2>::w(ky), accx);
+    }
+#pragma unroll
+    for (int o = 0; o < BZ; ++o) {
+      const int kz = q - 2 * o;   // offset of this plane for output Z0 + o
+      if (kz < -2 || kz > 2) continue;
+      acc[o] = cfmar<T>(acc[o], RW<2>::w(kz), accy);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < BZ; ++o)
+    if (o < zl) fc[gc.idx(X, Y, Z0 + o)] = acc[o];
+}
+
+// 3D prolongation + correction with BZ coarse planes per thread: the 3 x 3 coarse window of a
+// coarse plane is loaded once and reused by the (up to) 3 coarse planes around it; the fine
+// children 2J + {0,1}^3 of each coarse node get exactly k_prolong_block's sums.  One rank.
+template <typename TU, int PR, int BZ>
+__global__ void __launch_bounds__(256) k_prolong3_z(Geo gf, Geo gc, const double2 *__restrict__ e,
+                                                    const cplx<TU> *u, cplx<TU> *u_out) {
+  HMG_PDL_PROLOGUE();
+  using T = double;
+  const int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int Z0 = blockIdx.z * BZ;
+  if (X >= gc.n[0] || Y >= gc.n[1] || Z0 >= gc.n[2]) return;
+  auto plane = [&](int Z, cplx<T> (&c)[3][3]) {
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) c[dy][dx] = e[gc.idx(X - 1 + dx, Y - 1 + dy, Z)];
+  };
+  auto wt = [](int p, int k) -> double {
+    if (p == 0) return PR == 2 ? (k == 1 ? 0.75 : 0.125) : (k == 1 ? 1.0 : 0.0);
+    return k == 0 ? 0.0 : 0.5;
+  };
+  cplx<T> c[3][3][3];   // coarse planes Z-1, Z, Z+1
+  plane(Z0 - 1, c[0]);
+  plane(Z0, c[1]);
+  for (int o = 0; o < BZ; ++o) {
+    const int Z = Z0 + o;
+    if (Z >= gc.n[2]) break;
+    plane(Z + 1, c[2]);
+#pragma unroll
+    for (int pz = 0; pz < 2; ++pz)
+#pragma unroll
+      for (int py = 0; py < 2; ++py)
+#pragma unroll
+        for (int px = 0; px < 2; ++px) {
+          const int fx = 2 * X + px, fy = 2 * Y + py, fz = 2 * Z + pz;
+          if (fx >= gf.n[0] || fy >= gf.n[1] || fz >= gf.n[2]) continue;
+          cplx<T> acc = mkc<T>(0, 0);
+#pragma unroll
+          for (int dz = 0; dz < 3; ++dz) {
+            const double wz = wt(pz, dz);
+            if (wz == 0.0) continue;
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy) {
+              const double wy = wt(py, dy);
+              if (wy == 0.0) continue;
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx) {
+                const double wx = wt(px, dx);
+                if (wx == 0.0) continue;
+                acc = cfmar<T>(acc, wx * wy * wz, c[dz][dy][dx]);
+              }
+            }
+          }
+          const int64_t i = gf.idx(fx, fy, fz);
+          u_out[i] = ccast<TU, T>(cadd<T>(ccast<T, TU>(u[i]), acc));
+        }
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        c[0][dy][dx] = c[1][dy][dx];
+        c[1][dy][dx] = c[2][dy][dx];
+      }
+  }
+}
+
 // Prolongation + correction  u_out = u + P e  (Alg. 2.1 step 4), coarse-node parallel: the thread of coarse node J writes
 // the 2^d fine nodes 2J + {0,1}^d (global parity), loading its 3^d coarse
 // neighbourhood once (instead of up to 3^d loads per fine node).  Fine nodes

@@ -75,3 +75,39 @@ def _homog(cells, h, omega):
     gamma = media.sponge_gamma(cells, 4, 2.0 * omega)
     q = media.point_source(cells, h)
     return kappa, gamma, omega, q
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("cells,intergrid", [((20, 12, 68), "levdep"), ((24, 16, 36), "linear")])
+def test_zblock3_transfers_bit_identical(monkeypatch, dtype, cells, intergrid):
+    """3D restriction (fine level, 4 coarse planes per thread, each fine plane reduced once) and
+    prolongation (4 coarse planes per thread, coarse windows reused) against the per-node kernels
+    (HMG_NO_ZBLOCK3=1): bit-identical restrictions, prolongations, V-cycles; ragged plane counts."""
+    import torch
+    from paper_2511_16808_b200 import hmg, media
+    p = problem(3, cells)
+    opts = hmg.Options(dim=3, cells=p.cells, h=p.h, levels=3, smoother="element", intergrid=intergrid,
+                       damping=DAMPING[(3, "element")], dtype=dtype)
+    monkeypatch.delenv("HMG_NO_ZBLOCK3", raising=False)
+    ga = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.5)
+    monkeypatch.setenv("HMG_NO_ZBLOCK3", "1")
+    gb = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, 0.5)
+    monkeypatch.delenv("HMG_NO_ZBLOCK3")
+    cdt = torch.complex64 if dtype == "c64" else torch.complex128
+    for lvl in range(2):
+        nf, nc = ga.level_nodes(lvl)[0], ga.level_nodes(lvl + 1)[0]
+        r = torch.from_numpy(media.random_complex(nf, 1 + lvl)).to(cdt).cuda()
+        ca, cb = torch.zeros(nc, dtype=cdt, device="cuda"), torch.zeros(nc, dtype=cdt, device="cuda")
+        ga.restrict(r, ca, level=lvl)
+        gb.restrict(r, cb, level=lvl)
+        assert torch.equal(ca, cb), lvl
+        e = torch.from_numpy(media.random_complex(nc, 5 + lvl)).to(cdt).cuda()
+        ua, ub = r.clone(), r.clone()
+        ga.prolong_add(e, ua, level=lvl)
+        gb.prolong_add(e, ub, level=lvl)
+        assert torch.equal(ua, ub), lvl
+    q = torch.from_numpy(p.q.ravel()).to(cdt).cuda()
+    za, zb = torch.zeros_like(q), torch.zeros_like(q)
+    ga.vcycle(q, za)
+    gb.vcycle(q, zb)
+    assert torch.equal(za, zb)
