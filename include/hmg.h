@@ -255,6 +255,14 @@ HMG_API int hmg_copy_stencil(const hmg_hierarchy *hier, int level, double *out, 
  * heterogeneous medium, the coarsest level, or HMG_NO_UNIFORM=1 at build), -1 on
  * bad arguments.  lo/hi may be NULL. */
 HMG_API int64_t hmg_uniform_box(const hmg_hierarchy *hier, int level, int64_t lo[3], int64_t hi[3]);
+/* Coefficient dictionaries: the number of distinct coefficient
+ * vectors of level `level`'s stored stencil (coef_classes; levels >= 1) and of its
+ * assembled Vanka operator (bop_classes) when the kernels read them through a 2-byte
+ * class index per node and a class table instead of the per-node planes; 0 where
+ * the level keeps its planes (more than 65535 classes, e.g. a heterogeneous
+ * medium; the coarsest level; HMG_NO_DICT=1 at build).  Either pointer may be
+ * NULL.  Returns 0, or -1 on bad arguments. */
+HMG_API int hmg_dict_classes(const hmg_hierarchy *hier, int level, int *coef_classes, int *bop_classes);
 /* Kernel launches issued by this library since load (all entry points). */
 HMG_API int64_t hmg_launch_count(void);
 /* Opt-in per-kernel timing: after hmg_profile_begin(), every solve-path launch

@@ -427,8 +427,12 @@ template <typename TV, typename TK, int DIM, int R, int NR = 1, int BZ = 1>
 __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__restrict__ coef,
                                                    const cplx<TV> *__restrict__ x,
                                                    const cplx<TV> *__restrict__ f, cplx<TV> *__restrict__ y,
-                                                   int64_t bs, UBox ub, UCoef<kplanes<DIM, R>(), TV> uc) {
+                                                   int64_t bs, UBox ub, UCoef<kplanes<DIM, R>(), TV> uc,
+                                                   const unsigned short *__restrict__ cls,
+                                                   const cplx<TK> *__restrict__ tab) {
   HMG_PDL_PROLOGUE();
+  // cls != null: coefficient dictionary (k_dict.cuh): node i's coefficients are
+  // tab[cls[i]][0 .. K) (stored precision, converted like the planes)
   // NR right-hand sides at a stride of bs elements: each coefficient is read once
   // and applied to all of them (multi-RHS batches; same per-RHS arithmetic order).
   // BZ consecutive nodes along the slowest axis per thread (register blocking: each
@@ -480,8 +484,17 @@ __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__rest
   };
   // two copies of the unrolled loop behind a branch (not a per-coefficient select:
   // predicated-off loads and conversions would still take issue slots)
-  if (uni) run([&](int k, int) { return uc.c[k]; });
-  else run([&](int k, int o) { return ccast<T, TK>(coef[(int64_t)k * g.total + i0 + (int64_t)o * ps]); });
+  if (uni) {
+    run([&](int k, int) { return uc.c[k]; });
+  } else if (cls) {
+    constexpr int KP = kplanes<DIM, R>();
+    const cplx<TK> *cb[BZ];
+#pragma unroll
+    for (int o = 0; o < BZ; ++o) cb[o] = tab + (int64_t)cls[i0 + (int64_t)min(o, olast) * ps] * KP;
+    run([&](int k, int o) { return ccast<T, TK>(cb[o][k]); });
+  } else {
+    run([&](int k, int o) { return ccast<T, TK>(coef[(int64_t)k * g.total + i0 + (int64_t)o * ps]); });
+  }
 #pragma unroll
   for (int o = 0; o < BZ; ++o) {
     if (o > olast) break;
@@ -499,11 +512,13 @@ __global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__rest
 // BY outputs instead of (2R + 1) BY).  Input rows are visited in increasing order
 // and each output accumulates its terms in the offset order of k_stored_op, so
 // the per-node arithmetic (and result) is that of k_stored_op.
-template <int R, int BY = 1>
+template <int R, int BY = 1, bool DICT = false>
 __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *__restrict__ coef,
                                                           const double2 *__restrict__ x,
                                                           const double2 *__restrict__ f, double2 *__restrict__ y,
-                                                          UBox ub, UCoef<(2 * R + 1) * (2 * R + 1), double> uc) {
+                                                          UBox ub, UCoef<(2 * R + 1) * (2 * R + 1), double> uc,
+                                                          const unsigned short *__restrict__ cls,
+                                                          const float2 *__restrict__ tab) {
   HMG_PDL_PROLOGUE();
   using T = double;
   constexpr int W = 2 * R + 1;
@@ -550,6 +565,19 @@ __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *_
   };
   if (uni) {
     run([&](int k, int, double2 &k0, double2 &k1) { k0 = k1 = uc.c[k]; });
+  } else if (DICT) {   // coefficient dictionary (k_dict.cuh): tab[class][k]
+    const float2 *cb0[BY], *cb1[BY];
+#pragma unroll
+    for (int o = 0; o < BY; ++o) {
+      const int64_t i = i0 + (int64_t)min(o, ylast - iy0) * px;
+      cb0[o] = tab + (int64_t)cls[i] * (W * W);
+      cb1[o] = tab + (int64_t)cls[two ? i + 1 : i] * (W * W);
+    }
+    run([&](int k, int o, double2 &k0, double2 &k1) {
+      const float2 c0 = cb0[o][k], c1 = cb1[o][k];
+      k0 = mkc<T>(c0.x, c0.y);
+      k1 = mkc<T>(c1.x, c1.y);
+    });
   } else {
     run([&](int k, int o, double2 &k0, double2 &k1) {
       const float4 c2 = *reinterpret_cast<const float4 *>(coef + (int64_t)k * g.total + i0 + (int64_t)o * px);

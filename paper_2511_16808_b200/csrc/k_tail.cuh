@@ -26,6 +26,8 @@ struct TailLevel {
   double w;                  // damping
   const void *coef;          // stored stencil planes (TK)
   const void *bop;           // assembled Vanka operator planes (TK)
+  const unsigned short *ccls, *bcls;   // coefficient dictionaries (k_dict.cuh; null: the planes)
+  const void *ctab, *btab;             // their class tables [class][k] (TK)
   UBox ub;                   // uniform box
   const double2 *ucoef;      // its stencil / operator copies (device, fp64)
   const double2 *ubop;
@@ -71,19 +73,25 @@ __device__ __forceinline__ void tail_stored_node(const TailLevel &L, const doubl
   const Geo &g = L.geo;
   const int64_t i = g.idx(ix, iy, iz);
   const bool uni = L.ub.in(ix, iy, iz);
-  const cplx<TK> *coef = reinterpret_cast<const cplx<TK> *>(L.coef);
   constexpr int ZR = DIM == 3 ? R : 0;
+  constexpr int KP = (2 * R + 1) * (2 * R + 1) * (2 * ZR + 1);
+  // stored planes (stride total) or the node's dictionary entry (stride 1): one load path
+  const cplx<TK> *coef = L.ccls ? reinterpret_cast<const cplx<TK> *>(L.ctab) + (int64_t)L.ccls[i] * KP
+                                : reinterpret_cast<const cplx<TK> *>(L.coef) + i;
+  const int64_t cs = L.ccls ? 1 : g.total;
   cplx<T> acc = mkc<T>(0, 0);
-  int k = 0;
+  // two copies of the unrolled loop behind one branch, not a per-coefficient select
+  auto run = [&](auto ck) {
+    int k = 0;
 #pragma unroll
-  for (int oz = -ZR; oz <= ZR; ++oz)
+    for (int oz = -ZR; oz <= ZR; ++oz)
 #pragma unroll
-    for (int oy = -R; oy <= R; ++oy)
+      for (int oy = -R; oy <= R; ++oy)
 #pragma unroll
-      for (int ox = -R; ox <= R; ++ox, ++k) {
-        const cplx<T> c = uni ? L.ucoef[k] : ccast<T, TK>(coef[(int64_t)k * g.total + i]);
-        acc = cfma<T>(acc, c, x[i + g.delta(ox, oy, oz)]);
-      }
+        for (int ox = -R; ox <= R; ++ox, ++k) acc = cfma<T>(acc, ck(k), x[i + g.delta(ox, oy, oz)]);
+  };
+  if (uni) run([&](int k) { return L.ucoef[k]; });
+  else run([&](int k) { return ccast<T, TK>(coef[(int64_t)k * cs]); });
   y[i] = f ? csub<T>(f[i], acc) : acc;
 }
 
@@ -96,13 +104,18 @@ __device__ __forceinline__ void tail_vanka_node(const TailLevel &L, const double
   const Geo &g = L.geo;
   const int64_t j = g.idx(ix, iy, iz);
   const bool uni = L.ub.in(ix, iy, iz);
-  const cplx<TK> *B = reinterpret_cast<const cplx<TK> *>(L.bop);
+  const cplx<TK> *B = L.bcls ? reinterpret_cast<const cplx<TK> *>(L.btab) + (int64_t)L.bcls[j] * S::NB
+                             : reinterpret_cast<const cplx<TK> *>(L.bop) + j;
+  const int64_t bs = L.bcls ? 1 : g.total;
   cplx<T> acc = mkc<T>(0, 0);
-  static_for<0, S::NB>([&](auto P) {
-    constexpr int p = decltype(P)::value;
-    const cplx<T> b = uni ? L.ubop[p] : ccast<T, TK>(B[(int64_t)p * g.total + j]);
-    acc = cfma<T>(acc, b, r[j + g.delta(S::template dx<p>, S::template dy<p>, S::template dz<p>)]);
-  });
+  auto run = [&](auto bk) {
+    static_for<0, S::NB>([&](auto P) {
+      constexpr int p = decltype(P)::value;
+      acc = cfma<T>(acc, bk(p), r[j + g.delta(S::template dx<p>, S::template dy<p>, S::template dz<p>)]);
+    });
+  };
+  if (uni) run([&](int p) { return L.ubop[p]; });
+  else run([&](int p) { return ccast<T, TK>(B[(int64_t)p * bs]); });
   const T w = L.w;
   cplx<T> o;
   if (zero) {
@@ -193,8 +206,8 @@ __device__ void tail_stored_pass(const TailLevel &L, const double2 *x, const dou
 }
 
 // V(1,1) on levels l0 .. L-1 (zero initial guess on l0; lv[l0].f holds the right-hand side)
-template <typename TK, int DIM, int KIND>
-__global__ void __launch_bounds__(256) k_coarse_tail(const TailLevel *__restrict__ lv, int l0, int L,
+template <typename TK, int DIM, int KIND, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_coarse_tail(const TailLevel *__restrict__ lv, int l0, int L,
                                                      const double2 *__restrict__ ainv, unsigned *bar) {
   HMG_PDL_PROLOGUE();
   const unsigned nb = gridDim.x;

@@ -140,7 +140,9 @@ template <typename T, typename TK, int DIM, int KIND, int NR = 1>
 __global__ void __launch_bounds__(256) k_vanka_stencil(Geo g, const cplx<TK> *__restrict__ B,
                                                        const cplx<T> *__restrict__ r, const cplx<T> *u,
                                                        cplx<T> *u_out, T w, int zero, int64_t bs, UBox ub,
-                                                       UCoef<BStencil<DIM, KIND>::NB, T> uc) {
+                                                       UCoef<BStencil<DIM, KIND>::NB, T> uc,
+                                                       const unsigned short *__restrict__ cls,
+                                                       const cplx<TK> *__restrict__ tab) {
   HMG_PDL_PROLOGUE();
   HMG_NODE_IDX(g, ix, iy, iz);
   using S = BStencil<DIM, KIND>;
@@ -159,8 +161,14 @@ __global__ void __launch_bounds__(256) k_vanka_stencil(Geo g, const cplx<TK> *__
       for (int q = 0; q < NR; ++q) acc[q] = cfma<T>(acc[q], b, r[q * bs + o]);
     });
   };
-  if (uni) run([&](int p) { return uc.c[p]; });
-  else run([&](int p) { return ccast<T, TK>(B[(int64_t)p * g.total + j]); });
+  if (uni) {
+    run([&](int p) { return uc.c[p]; });
+  } else if (cls) {   // coefficient dictionary (k_dict.cuh): tab[class][p]
+    const cplx<TK> *cb = tab + (int64_t)cls[j] * S::NB;
+    run([&](int p) { return ccast<T, TK>(cb[p]); });
+  } else {
+    run([&](int p) { return ccast<T, TK>(B[(int64_t)p * g.total + j]); });
+  }
   // explicit fma / mul: the same rounding in every batch-width instantiation
   // (left to the compiler, u + w acc is contracted in some and not in others)
 #pragma unroll
@@ -184,7 +192,9 @@ template <typename T, typename TK, int DIM, int KIND, int BZ>
 __global__ void __launch_bounds__(256) k_vanka_stencil_blk(Geo g, const cplx<TK> *__restrict__ B,
                                                            const cplx<T> *__restrict__ r, const cplx<T> *u,
                                                            cplx<T> *u_out, T w, int zero, UBox ub,
-                                                           UCoef<BStencil<DIM, KIND>::NB, T> uc) {
+                                                           UCoef<BStencil<DIM, KIND>::NB, T> uc,
+                                                           const unsigned short *__restrict__ cls,
+                                                           const cplx<TK> *__restrict__ tab) {
   HMG_PDL_PROLOGUE();
   using S = BStencil<DIM, KIND>;
   const int ix = blockIdx.x * blockDim.x + threadIdx.x;
@@ -219,8 +229,16 @@ __global__ void __launch_bounds__(256) k_vanka_stencil_blk(Geo g, const cplx<TK>
       }
     }
   };
-  if (uni) run([&](int p, int) { return uc.c[p]; });
-  else run([&](int p, int o) { return ccast<T, TK>(B[(int64_t)p * g.total + j0 + (int64_t)o * ps]); });
+  if (uni) {
+    run([&](int p, int) { return uc.c[p]; });
+  } else if (cls) {   // coefficient dictionary (k_dict.cuh): tab[class][p]
+    const cplx<TK> *cb[BZ];
+#pragma unroll
+    for (int o = 0; o < BZ; ++o) cb[o] = tab + (int64_t)cls[j0 + (int64_t)min(o, olast) * ps] * S::NB;
+    run([&](int p, int o) { return ccast<T, TK>(cb[o][p]); });
+  } else {
+    run([&](int p, int o) { return ccast<T, TK>(B[(int64_t)p * g.total + j0 + (int64_t)o * ps]); });
+  }
 #pragma unroll
   for (int o = 0; o < BZ; ++o) {
     if (o > olast) break;

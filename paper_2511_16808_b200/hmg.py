@@ -75,6 +75,7 @@ _sigs = {
     "hmg_stencil_radius": ([_vp, _i], _i),
     "hmg_copy_stencil": ([_vp, _i, ctypes.POINTER(_d), _i64], _i),
     "hmg_uniform_box": ([_vp, _i, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i64),
+    "hmg_dict_classes": ([_vp, _i, ctypes.POINTER(_i), ctypes.POINTER(_i)], _i),
     "hmg_launch_count": ([], _i64),
     "hmg_profile_begin": ([], None),
     "hmg_profile_report": ([], ctypes.c_char_p),
@@ -330,6 +331,14 @@ class Hierarchy:
         if n < 0:
             raise HmgError(EINVAL, "level out of range")
         return int(n), tuple(lo[a] for a in range(self.opts.dim)), tuple(hi[a] for a in range(self.opts.dim))
+
+    def dict_classes(self, level):
+        """(stencil classes, Vanka-operator classes) of the level's coefficient
+        dictionaries; 0 where the planes are read."""
+        cn, bn = ctypes.c_int(), ctypes.c_int()
+        if _lib.hmg_dict_classes(self._h, level, ctypes.byref(cn), ctypes.byref(bn)) != 0:
+            raise HmgError(EINVAL, "level out of range")
+        return cn.value, bn.value
 
     def stencil_radius(self, level):
         return int(_lib.hmg_stencil_radius(self._h, level))

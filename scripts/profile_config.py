@@ -19,6 +19,8 @@ def main():
     from paper_2511_16808_b200 import hmg, media
     if a.config == 3:
         p, kw = media.config_problem(3), dict(levels=6, alpha=0.5, restart=10, dtype="c64")
+    elif a.config == 4:   # 1/2-scale replica, alpha frozen by reading R16
+        p, kw = media.config_problem(4, scale=2), dict(levels=6, alpha=0.6, restart=20, dtype="c64")
     elif a.config == 2:
         p, kw = media.config_problem(2), dict(levels=7, alpha=0.5, restart=20, dtype="c128")
     else:
@@ -37,7 +39,7 @@ def main():
     tot = sum(v["ms"] for v in prof.values())
     rows = sorted(prof.items(), key=lambda kv: -kv[1]["ms"])
     print(json.dumps({"config": a.config, "iterations": r.iterations, "kernel_ms": round(tot, 2)}))
-    for k, v in rows[:25]:
+    for k, v in rows[:40]:
         print(f"{k:32s} {v['ms']:9.2f} ms {v['launches']:6d} {v['bytes'] / (v['ms'] * 1e-3) / 1e9 if v['ms'] else 0:9.1f} GB/s")
 
 
