@@ -423,8 +423,8 @@ __global__ void __launch_bounds__(128) k_fine_resrestrict2d_march(Geo g, Geo gc,
 // TV = vector storage/arithmetic (fp64 on Galerkin levels), TK = coefficient storage.
 template <int DIM, int R> constexpr int kplanes() { return DIM == 3 ? (2 * R + 1) * (2 * R + 1) * (2 * R + 1) : (2 * R + 1) * (2 * R + 1); }
 
-template <typename TV, typename TK, int DIM, int R, int NR = 1, int BZ = 1>
-__global__ void __launch_bounds__(256) k_stored_op(Geo g, const cplx<TK> *__restrict__ coef,
+template <typename TV, typename TK, int DIM, int R, int NR = 1, int BZ = 1, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_stored_op(Geo g, const cplx<TK> *__restrict__ coef,
                                                    const cplx<TV> *__restrict__ x,
                                                    const cplx<TV> *__restrict__ f, cplx<TV> *__restrict__ y,
                                                    int64_t bs, UBox ub, UCoef<kplanes<DIM, R>(), TV> uc,

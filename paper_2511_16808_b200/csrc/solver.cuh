@@ -1356,7 +1356,12 @@ template <typename T> struct Solver : SolverBase {
         const int bz = (NR == 1 && Lv.geo.n[2] >= 64) ? bz_env : 1;
         dim3 grid4 = nl.grid;
         grid4.z = (Lv.geo.n[2] + 3) / 4;
-        if (bz == 4) {
+        // radius 2, 4 planes per thread: capped at 64 registers for 4 blocks per SM (measured on
+        // config 3 level 1: 46 -> 30 ms per solve on the same box; HMG_STORED_MINB=1: uncapped)
+        static const int minb = std::getenv("HMG_STORED_MINB") ? std::atoi(std::getenv("HMG_STORED_MINB")) : 4;
+        if (bz == 4 && minb >= 4 && Lv.r == 2) {
+          launch(k_stored_op<double, T, 3, 2, NR, 4, 4>, grid4, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv), ccl, ctb);
+        } else if (bz == 4) {
           if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR, 4>, grid4, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<27, double>(uv), ccl, ctb);
           else launch(k_stored_op<double, T, 3, 2, NR, 4>, grid4, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv), ccl, ctb);
         } else {
