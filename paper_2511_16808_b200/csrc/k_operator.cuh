@@ -166,14 +166,17 @@ __global__ void __launch_bounds__(256) k_fine_op2d_pair(Geo g, const cplx<TSG> *
 // k_fine_op2d_pair.  Same per-node grouping of the stencil sums as fine_op_node:
 // bit-identical to k_fine_op / k_fine_op2d_pair (tests/test_gpu_march.py).
 constexpr int FM_STRIP = 60;
-template <int KIND, typename TSG, int SEG, int PD>
+// TC: arithmetic (double: the FGMRES matvec and the fp64 model; float: the fp32 cycle residual
+// of DESIGN.md §4.1, fp32 sigma only)
+template <int KIND, typename TSG, int SEG, int PD, typename TC = double>
 __global__ void __launch_bounds__(128) k_fine_op2d_march(Geo g, const cplx<TSG> *__restrict__ sig, double alpha,
                                                          double ih2, const float2 *__restrict__ x,
                                                          const float2 *__restrict__ f, float2 *__restrict__ y, UBox ub,
                                                          double2 us) {
   HMG_PDL_PROLOGUE();
   using W = FineW<2, KIND>;
-  using CC = double2;
+  using CC = cplx<TC>;
+  static_assert(sizeof(TC) == 8 || sizeof(TSG) == 4, "fp32 arithmetic with fp32 sigma only");
   const int lane = threadIdx.x & 31;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nstrips = (g.n[0] + FM_STRIP - 1) / FM_STRIP;
@@ -217,19 +220,21 @@ __global__ void __launch_bounds__(128) k_fine_op2d_march(Geo g, const cplx<TSG> 
   };
 #pragma unroll
   for (int k = 0; k < PD; ++k) issue(k);
-  const CC z = make_double2(0, 0);
+  const CC z = mkc<TC>(0, 0);
+  const TC alp = (TC)alpha, ih2c = (TC)ih2;
+  const CC usc = mkc<TC>((TC)us.x, (TC)us.y);
   // rows b-2 (a) and b-1 (b): this lane's pair and its west / east neighbours (each row is
   // shuffled once, when it arrives, and rolls with the window)
   CC a0 = z, a1 = z, b0 = z, b1 = z, aw = z, ae = z, bw = z, be = z;
-  auto shl = [](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
-  auto shr = [](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
+  auto shl = [](auto v) { return __shfl_up_sync(0xffffffffu, v, 1); };
+  auto shr = [](auto v) { return __shfl_down_sync(0xffffffffu, v, 1); };
   for (int it = 0; it < nrows; ++it) {
     issue(it + PD);
     asm volatile("cp.async.wait_group %0;\n" ::"n"(PD) : "memory");
     const float4 *sl = ring + (it % NST) * NW * 32 + lane;
     const float4 xv = sl[0];
-    const CC c0 = make_double2(xv.x, xv.y), c1 = make_double2(xv.z, xv.w);   // row b
-    const CC cw = make_double2(shl(c1.x), shl(c1.y)), ce = make_double2(shr(c0.x), shr(c0.y));
+    const CC c0 = mkc<TC>(xv.x, xv.y), c1 = mkc<TC>(xv.z, xv.w);   // row b
+    const CC cw = mkc<TC>(shl(c1.x), shl(c1.y)), ce = mkc<TC>(shr(c0.x), shr(c0.y));
     if (it >= 2) {
       // output row yo = b - 1: rows a (yo - 1), b (yo), c (yo + 1); west of node 0 and east
       // of node 1 from the neighbour lanes
@@ -238,27 +243,29 @@ __global__ void __launch_bounds__(128) k_fine_op2d_march(Geo g, const cplx<TSG> 
         const float4 *sb = ring + ((it - 1) % NST) * NW * 32 + lane;   // row yo's f and sigma
         CC sg0, sg1;
         if (urow(yo)) {
-          sg0 = sg1 = us;
+          sg0 = sg1 = usc;
         } else if (SW == 1) {
           const float4 v = sb[2 * 32];
-          sg0 = make_double2(v.x, v.y);
-          sg1 = make_double2(v.z, v.w);
+          sg0 = mkc<TC>(v.x, v.y);
+          sg1 = mkc<TC>(v.z, v.w);
         } else {
           // the pair's two fp64 sigma values are this lane's words 2 and 3 (32 float4 apart)
-          sg0 = *reinterpret_cast<const double2 *>(sb + 2 * 32);
-          sg1 = *reinterpret_cast<const double2 *>(sb + 3 * 32);
+          const double2 d0 = *reinterpret_cast<const double2 *>(sb + 2 * 32);
+          const double2 d1 = *reinterpret_cast<const double2 *>(sb + 3 * 32);
+          sg0 = mkc<TC>((TC)d0.x, (TC)d0.y);
+          sg1 = mkc<TC>((TC)d1.x, (TC)d1.y);
         }
-        auto node = [&](CC cc, CC w_, CC e_, CC n_, CC s_, CC nw, CC ne, CC sw, CC se_, CC sgm, double fx, double fy) {
-          const CC sf = cadd<double>(cadd<double>(w_, e_), cadd<double>(n_, s_));
-          CC Lx = cscale<double>(cc, W::Lc);
-          Lx = cfmar<double>(Lx, W::Lf, sf);
-          if (W::Le != 0.0) Lx = cfmar<double>(Lx, W::Le, cadd<double>(cadd<double>(nw, ne), cadd<double>(sw, se_)));
-          Lx = cscale<double>(Lx, ih2);
-          CC Mx = cscale<double>(cc, W::Mc);
-          if (W::Mf != 0.0) Mx = cfmar<double>(Mx, W::Mf, sf);
-          sgm.y = fma(-alpha, sgm.x, sgm.y);
-          const CC Ax = csub<double>(Lx, cmul<double>(sgm, Mx));
-          return f ? csub<double>(make_double2(fx, fy), Ax) : Ax;
+        auto node = [&](CC cc, CC w_, CC e_, CC n_, CC s_, CC nw, CC ne, CC sw, CC se_, CC sgm, TC fx, TC fy) {
+          const CC sf = cadd<TC>(cadd<TC>(w_, e_), cadd<TC>(n_, s_));
+          CC Lx = cscale<TC>(cc, (TC)W::Lc);
+          Lx = cfmar<TC>(Lx, (TC)W::Lf, sf);
+          if (W::Le != 0.0) Lx = cfmar<TC>(Lx, (TC)W::Le, cadd<TC>(cadd<TC>(nw, ne), cadd<TC>(sw, se_)));
+          Lx = cscale<TC>(Lx, ih2c);
+          CC Mx = cscale<TC>(cc, (TC)W::Mc);
+          if (W::Mf != 0.0) Mx = cfmar<TC>(Mx, (TC)W::Mf, sf);
+          sgm.y = fma(-alp, sgm.x, sgm.y);
+          const CC Ax = csub<TC>(Lx, cmul<TC>(sgm, Mx));
+          return f ? csub<TC>(mkc<TC>(fx, fy), Ax) : Ax;
         };
         float4 fv = make_float4(0, 0, 0, 0);
         if (f) fv = sb[32];
@@ -287,7 +294,9 @@ __global__ void __launch_bounds__(128) k_fine_op2d_march(Geo g, const cplx<TSG> 
 // bit-identical to the residual kernel followed by k_restrict_pair.  Coarse rows I with
 // 2I in [y0, y1) (y0 even) belong to the segment.
 constexpr int RR_STRIP = 56;
-template <int KIND, int SEG, int PD>
+// TC: arithmetic of the residual (double: k_fine_op2d_march's; float: the fp32 cycle residual of
+// DESIGN.md §4.1); the restriction is fp64 either way
+template <int KIND, int SEG, int PD, typename TC = double>
 __global__ void __launch_bounds__(128) k_fine_resrestrict2d_march(Geo g, Geo gc, const float2 *__restrict__ sig,
                                                                   double alpha, double ih2,
                                                                   const float2 *__restrict__ x,
@@ -296,6 +305,7 @@ __global__ void __launch_bounds__(128) k_fine_resrestrict2d_march(Geo g, Geo gc,
   HMG_PDL_PROLOGUE();
   using W = FineW<2, KIND>;
   using CC = double2;
+  using CR = cplx<TC>;
   static_assert(SEG % 2 == 0, "segments start on even rows");
   const int lane = threadIdx.x & 31;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -342,9 +352,12 @@ __global__ void __launch_bounds__(128) k_fine_resrestrict2d_march(Geo g, Geo gc,
 #pragma unroll
   for (int k = 0; k < PD; ++k) issue(k);
   const CC z = make_double2(0, 0);
-  CC a0 = z, a1 = z, b0 = z, b1 = z, aw = z, ae = z, bw = z, be = z;
-  auto shl = [](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
-  auto shr = [](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
+  const CR zr = mkc<TC>(0, 0);
+  CR a0 = zr, a1 = zr, b0 = zr, b1 = zr, aw = zr, ae = zr, bw = zr, be = zr;
+  auto shl = [](auto v) { return __shfl_up_sync(0xffffffffu, v, 1); };
+  auto shr = [](auto v) { return __shfl_down_sync(0xffffffffu, v, 1); };
+  const TC alp = (TC)alpha, ih2c = (TC)ih2;
+  const CR usr = mkc<TC>((TC)us.x, (TC)us.y);
   CC P = z, Q = z;   // y-pass accumulators of coarse rows I0 - 1 and I0 (see below)
   const double w2 = 0.0625, w1 = 0.25, w0 = 0.375;   // RW<2>::w(+-2), (+-1), 0
   for (int it = 0; it < nrows; ++it) {
@@ -352,53 +365,56 @@ __global__ void __launch_bounds__(128) k_fine_resrestrict2d_march(Geo g, Geo gc,
     asm volatile("cp.async.wait_group %0;\n" ::"n"(PD) : "memory");
     const float4 *sl = ring + (it % NST) * NW * 32 + lane;
     const float4 xv = sl[0];
-    const CC c0 = make_double2(xv.x, xv.y), c1 = make_double2(xv.z, xv.w);
-    const CC cw = make_double2(shl(c1.x), shl(c1.y)), ce = make_double2(shr(c0.x), shr(c0.y));
+    const CR c0 = mkc<TC>(xv.x, xv.y), c1 = mkc<TC>(xv.z, xv.w);
+    const CR cw = mkc<TC>(shl(c1.x), shl(c1.y)), ce = mkc<TC>(shr(c0.x), shr(c0.y));
     if (it >= 2) {
       const int b = ybeg + it - 1;   // residual row (rows a = b-1, b, c = b+1)
       float2 r0 = make_float2(0, 0), r1 = make_float2(0, 0);
       if (rlane && b >= 0 && b < g.n[1]) {
         const float4 *sb = ring + ((it - 1) % NST) * NW * 32 + lane;   // row b's f and sigma
-        CC sg0, sg1;
+        CR sg0, sg1;
         if (urow(b)) {
-          sg0 = sg1 = us;
+          sg0 = sg1 = usr;
         } else {
           const float4 v = sb[2 * 32];
-          sg0 = make_double2(v.x, v.y);
-          sg1 = make_double2(v.z, v.w);
+          sg0 = mkc<TC>(v.x, v.y);
+          sg1 = mkc<TC>(v.z, v.w);
         }
         const float4 fv = sb[32];
-        auto node = [&](CC cc, CC w_, CC e_, CC n_, CC s_, CC nw, CC ne, CC sw, CC se_, CC sgm, double fx, double fy) {
-          const CC sf = cadd<double>(cadd<double>(w_, e_), cadd<double>(n_, s_));
-          CC Lx = cscale<double>(cc, W::Lc);
-          Lx = cfmar<double>(Lx, W::Lf, sf);
-          if (W::Le != 0.0) Lx = cfmar<double>(Lx, W::Le, cadd<double>(cadd<double>(nw, ne), cadd<double>(sw, se_)));
-          Lx = cscale<double>(Lx, ih2);
-          CC Mx = cscale<double>(cc, W::Mc);
-          if (W::Mf != 0.0) Mx = cfmar<double>(Mx, W::Mf, sf);
-          sgm.y = fma(-alpha, sgm.x, sgm.y);
-          return csub<double>(make_double2(fx, fy), csub<double>(Lx, cmul<double>(sgm, Mx)));
+        auto node = [&](CR cc, CR w_, CR e_, CR n_, CR s_, CR nw, CR ne, CR sw, CR se_, CR sgm, TC fx, TC fy) {
+          const CR sf = cadd<TC>(cadd<TC>(w_, e_), cadd<TC>(n_, s_));
+          CR Lx = cscale<TC>(cc, (TC)W::Lc);
+          Lx = cfmar<TC>(Lx, (TC)W::Lf, sf);
+          if (W::Le != 0.0) Lx = cfmar<TC>(Lx, (TC)W::Le, cadd<TC>(cadd<TC>(nw, ne), cadd<TC>(sw, se_)));
+          Lx = cscale<TC>(Lx, ih2c);
+          CR Mx = cscale<TC>(cc, (TC)W::Mc);
+          if (W::Mf != 0.0) Mx = cfmar<TC>(Mx, (TC)W::Mf, sf);
+          sgm.y = fma(-alp, sgm.x, sgm.y);
+          return csub<TC>(mkc<TC>(fx, fy), csub<TC>(Lx, cmul<TC>(sgm, Mx)));
         };
         if (in0) {
-          const CC o0 = node(b0, bw, b1, a0, c0, aw, a1, cw, c1, sg0, fv.x, fv.y);
+          const CR o0 = node(b0, bw, b1, a0, c0, aw, a1, cw, c1, sg0, fv.x, fv.y);
           r0 = make_float2((float)o0.x, (float)o0.y);
         }
         if (in1) {
-          const CC o1 = node(b1, b0, be, a1, c1, a0, ae, c0, ce, sg1, fv.z, fv.w);
+          const CR o1 = node(b1, b0, be, a1, c1, a0, ae, c0, ce, sg1, fv.z, fv.w);
           r1 = make_float2((float)o1.x, (float)o1.y);
         }
       }
       // x-pass of the restriction at coarse column X (fine 2X = x0): r at x0-2, x0-1 (left
       // lane's pair), x0, x0+1 (own), x0+2 (right lane's first)
-      const float2 lm2 = make_float2(__shfl_up_sync(0xffffffffu, r0.x, 1), __shfl_up_sync(0xffffffffu, r0.y, 1));
-      const float2 lm1 = make_float2(__shfl_up_sync(0xffffffffu, r1.x, 1), __shfl_up_sync(0xffffffffu, r1.y, 1));
-      const float2 rp2 = make_float2(__shfl_down_sync(0xffffffffu, r0.x, 1), __shfl_down_sync(0xffffffffu, r0.y, 1));
+      // the fp32-rounded residuals widened once per lane and shuffled as doubles (an
+      // F2F costs four DFMA issue slots on B200, a 64-bit shuffle two SHFL)
+      const CC R0 = ccast<double, float>(r0), R1 = ccast<double, float>(r1);
+      const CC lm2 = make_double2(shl(R0.x), shl(R0.y));
+      const CC lm1 = make_double2(shl(R1.x), shl(R1.y));
+      const CC rp2 = make_double2(shr(R0.x), shr(R0.y));
       CC hx = make_double2(0, 0);
-      hx = cfmar<double>(hx, w2, ccast<double, float>(lm2));
-      hx = cfmar<double>(hx, w1, ccast<double, float>(lm1));
-      hx = cfmar<double>(hx, w0, ccast<double, float>(r0));
-      hx = cfmar<double>(hx, w1, ccast<double, float>(r1));
-      hx = cfmar<double>(hx, w2, ccast<double, float>(rp2));
+      hx = cfmar<double>(hx, w2, lm2);
+      hx = cfmar<double>(hx, w1, lm1);
+      hx = cfmar<double>(hx, w0, R0);
+      hx = cfmar<double>(hx, w1, R1);
+      hx = cfmar<double>(hx, w2, rp2);
       // y-pass: fine row b = 2 I0 + ky.  Even b: completes row I0 - 1 (ky = +2), continues
       // I0 (ky = 0), opens I0 + 1 (ky = -2).  Odd b: ky = +1 for I0, -1 for I0 + 1.
       if ((b & 1) == 0) {

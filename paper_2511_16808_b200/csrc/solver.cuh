@@ -348,6 +348,15 @@ template <typename T> struct Solver : SolverBase {
   // padded box (capacity nrb_cap); the fine level runs per right-hand side
   int nrb = 1, nrb_cap = 1;
   cudaStream_t gstream = nullptr;
+  // side stream for the border instance of a split kernel pair (fork / join by events,
+  // also inside graph capture): both halves write disjoint nodes and read the same inputs
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool split_conc = true;   // HMG_NO_SPLIT_CONC=1 at build: the two halves back to back
+  // c64: the V-cycle's fine-level residuals in fp32 arithmetic (config 3 keeps its
+  // 70 iterations, 2.52 -> 2.40 ms per iteration; config 1 N = 4096 its 872, 1.440 -> 1.412 s;
+  // HMG_F64RES=1 at build: fp64 as before).  The FGMRES matvec and restart residual stay fp64.
+  bool f32res = true;
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   int nblk = 0;
   double *hpin = nullptr;
@@ -360,6 +369,9 @@ template <typename T> struct Solver : SolverBase {
     if (gev_in) cudaEventDestroy(gev_in);
     if (gev_out) cudaEventDestroy(gev_out);
     if (gstream) cudaStreamDestroy(gstream);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (hpin) cudaFreeHost(hpin);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -384,6 +396,8 @@ template <typename T> struct Solver : SolverBase {
     zblock3 = std::getenv("HMG_NO_ZBLOCK3") == nullptr;
     // measured: BZ = 2 helps the 3D element operator (config 3 level 0: 53 -> 50 ms per solve)
     // and hurts the 2D RB one (level 1 at N = 4096: 103 -> 117 ms)
+    split_conc = std::getenv("HMG_NO_SPLIT_CONC") == nullptr;
+    f32res = std::getenv("HMG_F64RES") == nullptr;
     vanka_bz = std::getenv("HMG_VANKA_BZ") ? std::atoi(std::getenv("HMG_VANKA_BZ")) : (opt.dim == 3 ? 2 : 1);
     if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
     lev.resize(L);
@@ -1135,6 +1149,10 @@ template <typename T> struct Solver : SolverBase {
       const double2 *sg = reinterpret_cast<const double2 *>(sgv);
       if (c4) go(k_fine_op2d_march<ST_COMPACT4, double, SEG, PD>, sg, 2);
       else go(k_fine_op2d_march<ST_FD2, double, SEG, PD>, sg, 2);
+    } else if (f32res) {   // the V-cycle's fine residual: fp32 arithmetic
+      const float2 *sg = reinterpret_cast<const float2 *>(sgv);
+      if (c4) go(k_fine_op2d_march<ST_COMPACT4, float, SEG, PD, float>, sg, 1);
+      else go(k_fine_op2d_march<ST_FD2, float, SEG, PD, float>, sg, 1);
     } else {
       const float2 *sg = reinterpret_cast<const float2 *>(sgv);
       if (c4) go(k_fine_op2d_march<ST_COMPACT4, float, SEG, PD>, sg, 1);
@@ -1163,6 +1181,11 @@ template <typename T> struct Solver : SolverBase {
       launch(kern, grid, block, (size_t)smem, s, g, gc, (const float2 *)sig.template as<C>(), alpha, ih2,
              (const float2 *)u, (const float2 *)f, (double2 *)fc, lev[0].ub, widen(usig));
     };
+    if (f32res) {   // fp32 residual arithmetic, restriction in fp64
+      if (opt.fine_stencil == HMG_COMPACT4) go(k_fine_resrestrict2d_march<ST_COMPACT4, SEG, PD, float>);
+      else go(k_fine_resrestrict2d_march<ST_FD2, SEG, PD, float>);
+      return true;
+    }
     if (opt.fine_stencil == HMG_COMPACT4) go(k_fine_resrestrict2d_march<ST_COMPACT4, SEG, PD>);
     else go(k_fine_resrestrict2d_march<ST_FD2, SEG, PD>);
     return true;
@@ -1235,9 +1258,14 @@ template <typename T> struct Solver : SolverBase {
       const bool c4 = opt.fine_stencil == HMG_COMPACT4;
       const UBox &ub = Lv.ub;
       if (fine2d_march(sg, false, a, ih2, xx, ff, yy, s)) return;
-      if (opt.dim == 2) {
+      if (opt.dim == 2 && f32res && std::is_same<T, float>::value) {   // fp32 cycle residual (§4.1)
+        if (c4) launch(k_fine_op<T, 2, ST_COMPACT4, T, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, (T)a, (T)ih2, xx, ff, yy, ub, usig);
+        else launch(k_fine_op<T, 2, ST_FD2, T, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, (T)a, (T)ih2, xx, ff, yy, ub, usig);
+      } else if (opt.dim == 2) {
         if (c4) launch(k_fine_op<T, 2, ST_COMPACT4, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy, ub, widen(usig));
         else launch(k_fine_op<T, 2, ST_FD2, double, T>, nl.grid, nl.block, 0, s, Lv.geo, sg, a, ih2, xx, ff, yy, ub, widen(usig));
+      } else if (f32res && std::is_same<T, float>::value) {   // 3D c64 cycle residual: fp32 arithmetic (§4.1)
+        fine3d<T, T, T>(Lv.geo, sg, (T)a, (T)ih2, xx, ff, yy, usig, s);
       } else {
         fine3d<T, double, T>(Lv.geo, sg, a, ih2, xx, ff, yy, widen(usig), s);
       }
@@ -1511,6 +1539,25 @@ template <typename T> struct Solver : SolverBase {
     }
   }
 
+  // fork: a stream ordered after everything enqueued on s so far (the side stream, or s itself
+  // when concurrency is off or profiling serialises the launches); join: s waits for it
+  cudaStream_t fork(cudaStream_t s) {
+    if (!split_conc || prof_active()) return s;
+    if (!side) {
+      CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ev_fork, s));
+    CK(cudaStreamWaitEvent(side, ev_fork, 0));
+    return side;
+  }
+  void join(cudaStream_t s, cudaStream_t s2) {
+    if (s2 == s) return;
+    CK(cudaEventRecord(ev_join, s2));
+    CK(cudaStreamWaitEvent(s, ev_join, 0));
+  }
+
   // Do the level's sweeps read neighbours of u inside one kernel?  Then they
   // must run out of place (other blocks may still read the old u).
   bool fused_sweep(int l) const { return l == 0 && rb_closed; }
@@ -1571,12 +1618,17 @@ template <typename T> struct Solver : SolverBase {
         if (Lv.ub.empty() || !rbfast) {
           if (zero) go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2>, 3);
           else go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3>, 5);
-        } else if (zero) {
-          go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2, 1>, 3);
-          go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2, 2>, 3);
         } else {
-          go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3, 1>, 5);
-          go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3, 2>, 5);
+          // the border warps (MODE 2: few, long generic marches) start first on the side stream
+          // and overlap the interior instance (MODE 1) instead of trailing it
+          cudaStream_t s0 = s, s2 = fork(s);
+          s = s2;
+          if (zero) go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2, 2>, 3);
+          else go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3, 2>, 5);
+          s = s0;
+          if (zero) go2(k_rb2d_march2<ST_COMPACT4, true, SEG, double, 4, PD, 2, 1>, 3);
+          else go2(k_rb2d_march2<ST_COMPACT4, false, SEG, float, 3, PD, 3, 1>, 5);
+          join(s, s2);
         }
         return;
       }
@@ -2298,6 +2350,8 @@ template <typename T> struct Solver : SolverBase {
     c->smarch = smarch;
     c->rrfuse = rrfuse;
     c->zblock3 = zblock3;
+    c->split_conc = split_conc;
+    c->f32res = f32res;
     c->tail_minb = tail_minb;
     c->usig = usig; c->uia = uia; c->uid = uid; c->usigd = usigd;
     c->sig = DBuf::view(sig);
