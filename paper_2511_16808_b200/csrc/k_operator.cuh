@@ -528,7 +528,35 @@ __global__ void __launch_bounds__(256, MINB) k_stored_op(Geo g, const cplx<TK> *
 // BY outputs instead of (2R + 1) BY).  Input rows are visited in increasing order
 // and each output accumulates its terms in the offset order of k_stored_op, so
 // the per-node arithmetic (and result) is that of k_stored_op.
-template <int R, int BY = 1, bool DICT = false>
+//
+// TILE (block 32 x 8): the block's 64 x 8 BY input tile plus a halo of 2 columns / R rows is
+// first copied to shared memory by cp.async (even and odd columns in separate arrays, so
+// the lanes' window reads are consecutive 16-byte words: conflict-free), and the x-window
+// is read from there: one global load per input element and block instead of a latency-
+// bound gather per thread (the arithmetic is unchanged: bit-identical).
+template <int BY, int R> struct Tile2D {
+  static constexpr int TH = 8 * BY + 2 * R, TC = 34;   // rows; 16-byte words per parity (68 columns)
+};
+template <int BY, int R>
+__device__ __forceinline__ void tile2d_load(const Geo &g, const double2 *__restrict__ x, double2 (*E)[34],
+                                            double2 (*O)[34]) {
+  constexpr int TH = Tile2D<BY, R>::TH;
+  const int X0 = blockIdx.x * 64, Y0 = blockIdx.y * 8 * BY;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int e = tid; e < TH * 68; e += 256) {
+    const int tr = e / 68, tc = e - tr * 68;
+    const int gx = X0 - 2 + tc, gy = Y0 - R + tr;
+    const bool ok = gx < g.n[0] + g.G && gy < g.n[1] + g.G;
+    double2 *dst = (tc & 1) ? &O[tr][tc >> 1] : &E[tr][tc >> 1];
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    const double2 *src = ok ? x + g.idx(gx, gy, 0) : x;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+}
+template <int R, int BY = 1, bool DICT = false, bool TILE = false>
 __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *__restrict__ coef,
                                                           const double2 *__restrict__ x,
                                                           const double2 *__restrict__ f, double2 *__restrict__ y,
@@ -538,6 +566,9 @@ __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *_
   HMG_PDL_PROLOGUE();
   using T = double;
   constexpr int W = 2 * R + 1;
+  constexpr int TH = TILE ? Tile2D<BY, R>::TH : 1;
+  __shared__ __align__(16) double2 tE[TILE ? TH : 1][34], tO[TILE ? TH : 1][34];
+  if (TILE) tile2d_load<BY, R>(g, x, tE, tO);
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int iy0 = (blockIdx.y * blockDim.y + threadIdx.y) * BY;
   const int ix = 2 * p;
@@ -560,10 +591,19 @@ __global__ void __launch_bounds__(256) k_stored_op2d_pair(Geo g, const float2 *_
 #pragma unroll
     for (int r = -R; r < BY + R; ++r) {
       if (r > rmax) break;
-      const double2 *row = x + i0 + (int64_t)r * px;
       double2 xw[2 * R + 2];
+      if (TILE) {   // tile row threadIdx.y * BY + r + R; column ix - R + c = tile column 2 tx + 2 - R + c
+        const int tr = threadIdx.y * BY + r + R, tx = threadIdx.x;
 #pragma unroll
-      for (int c = 0; c < 2 * R + 2; ++c) xw[c] = row[c - R];
+        for (int c = 0; c < 2 * R + 2; ++c) {
+          const int tc = 2 - R + c;   // >= 0 (R <= 2)
+          xw[c] = (tc & 1) ? tO[tr][tx + (tc >> 1)] : tE[tr][tx + (tc >> 1)];
+        }
+      } else {
+        const double2 *row = x + i0 + (int64_t)r * px;
+#pragma unroll
+        for (int c = 0; c < 2 * R + 2; ++c) xw[c] = row[c - R];
+      }
 #pragma unroll
       for (int o = 0; o < BY; ++o) {
         const int oy = r - o;   // offset of this input row for output row o

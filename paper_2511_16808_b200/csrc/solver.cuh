@@ -353,6 +353,10 @@ template <typename T> struct Solver : SolverBase {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool split_conc = true;   // HMG_NO_SPLIT_CONC=1 at build: the two halves back to back
+  // 2D Galerkin levels: the stored stencil from a shared-memory tile of x (HMG_NO_TILE2D=1 at
+  // build: the gather).  Measured at N = 4096: level-1 residual 134 -> 122 ms per solve; the
+  // same tiling of the Vanka operator was slower (92 -> 116 ms) and was dropped.
+  bool tile2d = true;
   // c64: the V-cycle's fine-level residuals in fp32 arithmetic (config 3 keeps its
   // 70 iterations, 2.52 -> 2.40 ms per iteration; config 1 N = 4096 its 872, 1.440 -> 1.412 s;
   // HMG_F64RES=1 at build: fp64 as before).  The FGMRES matvec and restart residual stay fp64.
@@ -397,6 +401,7 @@ template <typename T> struct Solver : SolverBase {
     // measured: BZ = 2 helps the 3D element operator (config 3 level 0: 53 -> 50 ms per solve)
     // and hurts the 2D RB one (level 1 at N = 4096: 103 -> 117 ms)
     split_conc = std::getenv("HMG_NO_SPLIT_CONC") == nullptr;
+    tile2d = std::getenv("HMG_NO_TILE2D") == nullptr;
     f32res = std::getenv("HMG_F64RES") == nullptr;
     vanka_bz = std::getenv("HMG_VANKA_BZ") ? std::atoi(std::getenv("HMG_VANKA_BZ")) : (opt.dim == 3 ? 2 : 1);
     if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
@@ -1342,6 +1347,16 @@ template <typename T> struct Solver : SolverBase {
         launch(kern, grid, block, 0, s, Lv.geo, c2, xx, ff, yy, Lv.ub, ucopy<9, double>(Lv.ucoef), ccl,
                reinterpret_cast<const float2 *>(ctb));
       };
+      if (tile2d && BY == 2) {   // shared-memory tile of x (k_stored_op2d_pair<..., TILE>)
+        if (ccl) {
+          if (Lv.r == 1) go1(k_stored_op2d_pair<1, 2, true, true>, 2);
+          else go(k_stored_op2d_pair<2, 2, true, true>, 2);
+        } else {
+          if (Lv.r == 1) go1(k_stored_op2d_pair<1, 2, false, true>, 2);
+          else go(k_stored_op2d_pair<2, 2, false, true>, 2);
+        }
+        return;
+      }
       if (ccl) {   // coefficient dictionary
         if (Lv.r == 1) {
           if (BY == 4) go1(k_stored_op2d_pair<1, 4, true>, 4);
@@ -2351,6 +2366,7 @@ template <typename T> struct Solver : SolverBase {
     c->rrfuse = rrfuse;
     c->zblock3 = zblock3;
     c->split_conc = split_conc;
+    c->tile2d = tile2d;
     c->f32res = f32res;
     c->tail_minb = tail_minb;
     c->usig = usig; c->uia = uia; c->uid = uid; c->usigd = usigd;

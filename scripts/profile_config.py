@@ -21,6 +21,8 @@ def main():
         p, kw = media.config_problem(3), dict(levels=6, alpha=0.5, restart=10, dtype="c64")
     elif a.config == 4:   # 1/2-scale replica, alpha frozen by reading R16
         p, kw = media.config_problem(4, scale=2), dict(levels=6, alpha=0.6, restart=20, dtype="c64")
+    elif a.config == 1:
+        p, kw = media.config_problem(1, n=4096), dict(levels=9, alpha=0.25, restart=20, dtype="c64")
     elif a.config == 2:
         p, kw = media.config_problem(2), dict(levels=7, alpha=0.5, restart=20, dtype="c128")
     else:
