@@ -447,16 +447,20 @@ def dry_run(args):
     """Rendezvous only (CPU): every rank reports itself, rank 0 the world size."""
     ws, rank, local = _dist()
     import torch.distributed as dist
+    rec = {"dry_run": True, "rank": rank, "world_size": ws, "local_rank": local, "gpus": args.gpus}
     if ws > 1:
         dist.init_process_group("gloo")
         t = __import__("torch").tensor([1])
         dist.all_reduce(t)
-        n = int(t.item())
+        rec["ranks_seen"] = int(t.item())
+        for r in range(ws):  # one rank at a time: the ranks share one stdout pipe
+            if r == rank:
+                os.write(1, (json.dumps(rec) + "\n").encode())
+            dist.barrier()
         dist.destroy_process_group()
     else:
-        n = 1
-    print(json.dumps({"dry_run": True, "rank": rank, "world_size": ws, "local_rank": local, "ranks_seen": n,
-                      "gpus": args.gpus}), flush=True)
+        rec["ranks_seen"] = 1
+        os.write(1, (json.dumps(rec) + "\n").encode())
 
 
 def main():
