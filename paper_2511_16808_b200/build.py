@@ -50,6 +50,20 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
+def _includes(path, seen=None):
+    """Transitive quoted includes of a source file (csrc/ and include/ only)."""
+    import re
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as fh:
+        for m in re.finditer(r'^\s*#\s*include\s+"([^"]+)"', fh.read(), re.M):
+            for base in (os.path.dirname(path), CSRC, os.path.join(ROOT, "include")):
+                _includes(os.path.join(base, m.group(1)), seen)
+    return seen
+
+
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
@@ -58,6 +72,12 @@ def build(force=False, verbose=False):
 
     def compile_one(src):
         obj = os.path.join(PKG, "build", os.path.basename(src) + ".o")
+        # per-object incremental: an object newer than its source, every header it includes
+        # and this script is reused (the solver translation units take minutes)
+        if not force and os.path.exists(obj):
+            t = os.path.getmtime(obj)
+            if all(os.path.getmtime(d) <= t for d in list(_includes(src)) + [os.path.abspath(__file__)]):
+                return obj
         cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log = os.path.join(PKG, "build", os.path.basename(src) + ".ptxas.log")

@@ -53,6 +53,19 @@ __device__ __forceinline__ void tail_sync(unsigned *bar, unsigned nblocks) {
   __syncthreads();
 }
 
+// cluster variant: the whole tail runs as ONE thread-block cluster (gridDim = cluster size), so
+// the passes are separated by the hardware cluster barrier (release / acquire at cluster
+// scope orders the global-memory writes of one pass before the reads of the next) instead of
+// atomics on a global word -- a few hundred ns per pass instead of microseconds
+__device__ __forceinline__ void tail_sync_cluster() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <bool CLUSTER>
+__device__ __forceinline__ void tail_barrier(unsigned *bar, unsigned nblocks) {
+  if constexpr (CLUSTER) tail_sync_cluster();
+  else tail_sync(bar, nblocks);
+}
+
 template <typename F>
 __device__ __forceinline__ void tail_nodes(const Geo &g, F &&fn) {
   const int64_t n = g.nodes();
@@ -206,8 +219,8 @@ __device__ void tail_stored_pass(const TailLevel &L, const double2 *x, const dou
 }
 
 // V(1,1) on levels l0 .. L-1 (zero initial guess on l0; lv[l0].f holds the right-hand side)
-template <typename TK, int DIM, int KIND, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_coarse_tail(const TailLevel *__restrict__ lv, int l0, int L,
+template <typename TK, int DIM, int KIND, int MINB = 1, int NT = 256, bool CLUSTER = false>
+__global__ void __launch_bounds__(NT, MINB) k_coarse_tail(const TailLevel *__restrict__ lv, int l0, int L,
                                                      const double2 *__restrict__ ainv, unsigned *bar) {
   HMG_PDL_PROLOGUE();
   const unsigned nb = gridDim.x;
@@ -215,12 +228,12 @@ __global__ void __launch_bounds__(256, MINB) k_coarse_tail(const TailLevel *__re
     const TailLevel &A = lv[l], &B = lv[l + 1];
     // zero-guess pre-smoothing u = w B f
     tail_nodes(A.geo, [&](int a, int b, int c) { tail_vanka_node<TK, DIM, KIND>(A, A.f, nullptr, A.u, 1, a, b, c); });
-    tail_sync(bar, nb);
+    tail_barrier<CLUSTER>(bar, nb);
     tail_stored_pass<TK, DIM, KIND>(A, A.u, A.f, A.r_);   // r = f - A u
-    tail_sync(bar, nb);
+    tail_barrier<CLUSTER>(bar, nb);
     if (A.rR == 1) tail_nodes(B.geo, [&](int a, int b, int c) { tail_restrict_node<DIM, 1>(A.geo, B.geo, A.r_, B.f, a, b, c); });
     else tail_nodes(B.geo, [&](int a, int b, int c) { tail_restrict_node<DIM, 2>(A.geo, B.geo, A.r_, B.f, a, b, c); });
-    tail_sync(bar, nb);
+    tail_barrier<CLUSTER>(bar, nb);
   }
   {   // coarsest: e = A_L^{-1} f, one warp per row (k_coarse_gemv's lane order and warp sum)
     const TailLevel &C = lv[L - 1];
@@ -243,18 +256,24 @@ __global__ void __launch_bounds__(256, MINB) k_coarse_tail(const TailLevel *__re
         C.u[g.idx(rx, ry, rz)] = make_double2(sx, sy);
       }
     }
-    tail_sync(bar, nb);
+    tail_barrier<CLUSTER>(bar, nb);
   }
   for (int l = L - 2; l >= l0; --l) {
     const TailLevel &A = lv[l], &B = lv[l + 1];
     if (A.rP == 1) tail_nodes(B.geo, [&](int a, int b, int c) { tail_prolong_node<DIM, 1>(A.geo, B.geo, B.u, A.u, a, b, c); });
     else tail_nodes(B.geo, [&](int a, int b, int c) { tail_prolong_node<DIM, 2>(A.geo, B.geo, B.u, A.u, a, b, c); });
-    tail_sync(bar, nb);
+    tail_barrier<CLUSTER>(bar, nb);
     tail_stored_pass<TK, DIM, KIND>(A, A.u, A.f, A.r_);   // post-smoothing: r = f - A u
-    tail_sync(bar, nb);
+    tail_barrier<CLUSTER>(bar, nb);
     tail_nodes(A.geo, [&](int a, int b, int c) { tail_vanka_node<TK, DIM, KIND>(A, A.r_, A.u, A.u, 0, a, b, c); });
-    if (l > l0) tail_sync(bar, nb);
+    if (l > l0) tail_barrier<CLUSTER>(bar, nb);
   }
 }
+
+// the cluster instantiations live in their own translation unit (tail_cluster.cu): the kernel
+// of the given storage precision / dimension / patch kind, launched with TAIL_CL_NT threads per
+// block and gridDim = cluster size (null: not instantiated)
+constexpr int TAIL_CL_NT = 512;
+void *tail_cluster_fn(bool fp64_storage, int dim, int kind);
 
 }  // namespace hmg

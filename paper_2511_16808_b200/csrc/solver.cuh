@@ -624,11 +624,26 @@ template <typename T> struct Solver : SolverBase {
   // blocks per SM the tail is compiled for (HMG_TAIL_MINB=2 at build: a 128-register cap; measured
   // 22.9 vs 22.1 ms per config-3 solve for the uncapped 1)
   int tail_minb = 1;
+  // cluster tail: cluster size (0: the cooperative grid-barrier tail).  One thread-block cluster
+  // of 16 (8) blocks x TAIL_CL_NT threads runs the levels below HMG_TAIL_CLUSTER_NODES nodes with
+  // the hardware cluster barrier between passes.  Opt-in: bit-identical, but measured slower than
+  // the per-kernel graph (N = 4096 c64: levels >= 4 on a 16-block cluster 1.681 vs 1.604 ms per
+  // iteration, levels >= 5 1.616; 8 blocks 1.779): 16 SMs are too few for the passes themselves
+  int tail_cluster = 0;
+  int tail_kind() const {
+    switch (opt.smoother) {
+      case HMG_VANKA_RB: return PK_RB;
+      case HMG_VANKA_ELEMENT: return PK_ELEMENT;
+      case HMG_JACOBI: return PK_JACOBI;
+      default: return PK_PLUS;
+    }
+  }
   template <int DIM, int KIND> void *tail_kernel() const {
     return tail_minb == 1 ? (void *)k_coarse_tail<T, DIM, KIND, 1> : (void *)k_coarse_tail<T, DIM, KIND, 2>;
   }
   void *tail_fn() const {
     const int d = opt.dim;
+    if (tail_cluster) return tail_cluster_fn(sizeof(T) == 8, d, tail_kind());
     switch (opt.smoother) {
       case HMG_VANKA_RB: return tail_kernel<2, PK_RB>();
       case HMG_VANKA_ELEMENT: return d == 2 ? tail_kernel<2, PK_ELEMENT>() : tail_kernel<3, PK_ELEMENT>();
@@ -644,10 +659,41 @@ template <typename T> struct Solver : SolverBase {
     // faster (N = 4096: levels >= 4 in one tail launch 177 us per cycle, the solve 1.505 -> 1.543 s)
     const int64_t thr = std::getenv("HMG_TAIL_NODES") ? std::atoll(std::getenv("HMG_TAIL_NODES"))
                                                       : (opt.dim == 3 ? 300000 : 0);
-    if (thr <= 0 || L < 3 || (comm && comm->size > 1) || opt.cycle != 0 || opt.nu1 != 1 || opt.nu2 != 1) return;
+    const int64_t cthr = std::getenv("HMG_TAIL_CLUSTER_NODES") ? std::atoll(std::getenv("HMG_TAIL_CLUSTER_NODES"))
+                                                               : 0;
+    tail_cluster = 0;
+    if (L < 3 || (comm && comm->size > 1) || opt.cycle != 0 || opt.nu1 != 1 || opt.nu2 != 1) return;
     int l0 = -1;
-    for (int l = 1; l + 1 < L; ++l)
+    for (int l = 1; l + 1 < L && thr > 0; ++l)
       if (lev[l].geo.nodes() <= thr) { l0 = l; break; }
+    if (l0 < 0 && cthr > 0) {   // no grid-barrier tail: the cluster tail on the smaller levels
+      for (int l = 1; l + 1 < L; ++l)
+        if (lev[l].geo.nodes() <= cthr) { l0 = l; break; }
+      if (l0 >= 0) {
+        void *fn = tail_cluster_fn(sizeof(T) == 8, opt.dim, tail_kind());
+        const int want = std::getenv("HMG_TAIL_CLUSTER") ? std::atoi(std::getenv("HMG_TAIL_CLUSTER")) : 16;
+        for (int cs = want; fn && cs >= 2 && !tail_cluster; cs /= 2) {
+          if (cs > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            (void)cudaGetLastError();
+            continue;
+          }
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(cs);
+          cfg.blockDim = dim3(TAIL_CL_NT);
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = cs;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          int nc = 0;
+          if (cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) == cudaSuccess && nc >= 1) tail_cluster = cs;
+          else (void)cudaGetLastError();
+        }
+        if (!tail_cluster) l0 = -1;
+      }
+    }
     if (l0 < 0) return;
     std::vector<TailLevel> tl(L);
     std::vector<double2> uc;   // all uniform copies, offsets recorded per level
@@ -684,11 +730,15 @@ template <typename T> struct Solver : SolverBase {
     tail_lv.alloc(L * sizeof(TailLevel), s);
     CK(cudaMemcpyAsync(tail_lv.p, tl.data(), L * sizeof(TailLevel), cudaMemcpyHostToDevice, s));
     tail_bar.alloc(2 * sizeof(unsigned), s);
-    int per_sm = 0, dev = 0, sms = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_fn(), 256, 0));
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    tail_grid = std::max(1, std::min(per_sm, tail_minb)) * sms;   // co-resident (cooperative launch, launch_tail)
+    if (tail_cluster) {
+      tail_grid = tail_cluster;
+    } else {
+      int per_sm = 0, dev = 0, sms = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_fn(), 256, 0));
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      tail_grid = std::max(1, std::min(per_sm, tail_minb)) * sms;   // co-resident (cooperative launch, launch_tail)
+    }
     CK(cudaStreamSynchronize(s));
     tail_l0 = l0;
   }
@@ -701,12 +751,19 @@ template <typename T> struct Solver : SolverBase {
     // grid barrier needs it, also when other streams run tails concurrently); capturable
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(tail_grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(tail_cluster ? TAIL_CL_NT : 256);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    if (tail_cluster) {   // one cluster: the hardware co-schedules its blocks (no cooperative launch)
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = tail_cluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+    } else {
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+    }
     cfg.attrs = at;
     cfg.numAttrs = 1;
     const int pi = prof_before(s);

@@ -1,7 +1,8 @@
 """The persistent coarse tail (k_coarse_tail: the small levels of a one-rank
-V(1,1) cycle in one launch with a software grid barrier) against the per-kernel cycle
-(HMG_TAIL_NODES=0): the same per-node arithmetic, so V-cycles and FGMRES solves must be
-BIT-identical -- 2D RB and Element, 3D Element and Plus, both precisions, homogeneous (uniform
+V(1,1) cycle in one launch -- a cooperative grid with a software grid barrier, or ONE
+thread-block cluster of 16 / 8 blocks with the hardware cluster barrier) against the per-kernel
+cycle (HMG_TAIL_NODES=0, HMG_TAIL_CLUSTER_NODES=0): the same per-node arithmetic, so V-cycles and
+FGMRES solves must be BIT-identical -- 2D RB and Element, 3D Element and Plus, both precisions, homogeneous (uniform
 boxes) and heterogeneous media, and multi-RHS batches after a buffer reallocation."""
 import pytest
 
@@ -17,21 +18,32 @@ def _cuda():
         pytest.skip("needs a GPU")
 
 
-def _pair(monkeypatch, p, L, sm, dtype, alpha, thr="300000"):
+def _pair(monkeypatch, p, L, sm, dtype, alpha, thr="300000", mode="grid"):
+    """(hierarchy with the tail in `mode`, hierarchy with the per-kernel cycle); mode: "grid"
+    (cooperative launch, software barrier) or "cluster16" / "cluster8" (one cluster)."""
     from paper_2511_16808_b200 import hmg
     opts = hmg.Options(dim=p.dim, cells=p.cells, h=p.h, levels=L, smoother=sm, damping=DAMPING[(p.dim, sm)],
                        dtype=dtype)
-    monkeypatch.setenv("HMG_TAIL_NODES", thr)
+    if mode == "grid":
+        monkeypatch.setenv("HMG_TAIL_NODES", thr)
+        monkeypatch.setenv("HMG_TAIL_CLUSTER_NODES", "0")
+    else:
+        monkeypatch.setenv("HMG_TAIL_NODES", "0")
+        monkeypatch.setenv("HMG_TAIL_CLUSTER_NODES", thr)
+        monkeypatch.setenv("HMG_TAIL_CLUSTER", mode[len("cluster"):])
     ga = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, alpha)
     monkeypatch.setenv("HMG_TAIL_NODES", "0")
+    monkeypatch.setenv("HMG_TAIL_CLUSTER_NODES", "0")
     gb = hmg.Hierarchy(opts, p.kappa, p.omega, p.gamma, alpha)
-    monkeypatch.delenv("HMG_TAIL_NODES")
+    for k in ("HMG_TAIL_NODES", "HMG_TAIL_CLUSTER_NODES", "HMG_TAIL_CLUSTER"):
+        monkeypatch.delenv(k, raising=False)
     return ga, gb
 
 
+@pytest.mark.parametrize("mode", ["grid", "cluster16", "cluster8"])
 @pytest.mark.parametrize("case,dtype", [("2d_rb", "c64"), ("2d_rb", "c128"), ("2d_element", "c64"),
                                         ("2d_hetero", "c128"), ("3d_element", "c64"), ("3d_plus", "c128")])
-def test_tail_bit_identical(monkeypatch, case, dtype):
+def test_tail_bit_identical(monkeypatch, case, dtype, mode):
     import torch
     from paper_2511_16808_b200 import media
     if case == "2d_rb":
@@ -45,7 +57,7 @@ def test_tail_bit_identical(monkeypatch, case, dtype):
     else:
         p, L, sm, al, m = problem(3, (16, 16, 32)), 3, "plus", 0.65, 10
     # a threshold that puts every coarse level in the tail
-    ga, gb = _pair(monkeypatch, p, L, sm, dtype, al, thr="100000000")
+    ga, gb = _pair(monkeypatch, p, L, sm, dtype, al, thr="100000000", mode=mode)
     cdt = torch.complex64 if dtype == "c64" else torch.complex128
     q = torch.from_numpy(p.q.ravel()).to(cdt).cuda()
     for seed in (0, 1):
@@ -60,13 +72,14 @@ def test_tail_bit_identical(monkeypatch, case, dtype):
     assert ra.converged and ra.iterations == rb.iterations and torch.equal(xa, xb)
 
 
-def test_tail_after_batch_realloc(monkeypatch):
+@pytest.mark.parametrize("mode", ["grid", "cluster16"])
+def test_tail_after_batch_realloc(monkeypatch, mode):
     """A multi-RHS batch reallocates the coarse-level vectors; single solves afterwards still
     equal the per-kernel path (the tail's level table follows the new buffers)."""
     import torch
     from paper_2511_16808_b200 import media
     p = media.config_problem(0)
-    ga, gb = _pair(monkeypatch, p, 4, "rb", "c128", 0.15, thr="100000000")
+    ga, gb = _pair(monkeypatch, p, 4, "rb", "c128", 0.15, thr="100000000", mode=mode)
     q = torch.from_numpy(p.q.ravel()).cuda()
     Q = torch.stack([q, q.roll(3000)])
     X = torch.zeros_like(Q)
