@@ -466,8 +466,12 @@ __global__ void __launch_bounds__(256, MINB) k_stored_op(Geo g, const cplx<TK> *
   const int64_t ps = DIM == 3 ? g.pxy : g.px;   // slow-axis pitch
   const int slow0 = DIM == 3 ? iz : iy, nslow = DIM == 3 ? g.n[2] : g.n[1];
   const int olast = min(slow0 + BZ, nslow) - 1 - slow0;   // last valid output of the block
-  const bool uni = DIM == 3 ? ub.in(ix, iy, iz) && ub.in(ix, iy, iz + olast)
-                            : ub.in(ix, iy, 0) && ub.in(ix, iy + olast, 0);
+  bool uni = DIM == 3 ? ub.in(ix, iy, iz) && ub.in(ix, iy, iz + olast)
+                      : ub.in(ix, iy, 0) && ub.in(ix, iy + olast, 0);
+  // a warp with lanes on both sides of the box (an x-normal sponge face) would run BOTH copies of
+  // the unrolled loop; with a dictionary every lane can take its class's entry instead -- inside
+  // the box that is the box's own class, bitwise the uniform copy -- so such a warp runs one
+  if (cls && !__all_sync(__activemask(), uni)) uni = false;
   cplx<T> acc[BZ][NR];
 #pragma unroll
   for (int o = 0; o < BZ; ++o)

@@ -147,7 +147,11 @@ __global__ void __launch_bounds__(256) k_vanka_stencil(Geo g, const cplx<TK> *__
   HMG_NODE_IDX(g, ix, iy, iz);
   using S = BStencil<DIM, KIND>;
   const int64_t j = g.idx(ix, iy, iz);
-  const bool uni = ub.in(ix, iy, iz);   // B from the uniform-box copy (k_uniform.cuh)
+  bool uni = ub.in(ix, iy, iz);   // B from the uniform-box copy (k_uniform.cuh)
+  // a warp with lanes on both sides of the box (an x-normal sponge face) would run BOTH copies of
+  // the unrolled loop; with a dictionary every lane can take its class's entry instead -- inside
+  // the box that is the box's own class, bitwise the uniform copy -- so such a warp runs one
+  if (cls && !__all_sync(__activemask(), uni)) uni = false;
   cplx<T> acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = mkc<T>(0, 0);
@@ -206,8 +210,12 @@ __global__ void __launch_bounds__(256) k_vanka_stencil_blk(Geo g, const cplx<TK>
   const int64_t ps = DIM == 3 ? g.pxy : g.px;
   const int slow0 = DIM == 3 ? iz : iy, nslow = DIM == 3 ? g.n[2] : g.n[1];
   const int olast = min(slow0 + BZ, nslow) - 1 - slow0;
-  const bool uni = DIM == 3 ? ub.in(ix, iy, iz) && ub.in(ix, iy, iz + olast)
-                            : ub.in(ix, iy, 0) && ub.in(ix, iy + olast, 0);
+  bool uni = DIM == 3 ? ub.in(ix, iy, iz) && ub.in(ix, iy, iz + olast)
+                      : ub.in(ix, iy, 0) && ub.in(ix, iy + olast, 0);
+  // a warp with lanes on both sides of the box (an x-normal sponge face) would run BOTH copies of
+  // the unrolled loop; with a dictionary every lane can take its class's entry instead -- inside
+  // the box that is the box's own class, bitwise the uniform copy -- so such a warp runs one
+  if (cls && !__all_sync(__activemask(), uni)) uni = false;
   constexpr int SR = 2;   // |slow offset| <= 2 for every patch kind
   cplx<T> acc[BZ];
 #pragma unroll
