@@ -201,8 +201,15 @@ __global__ void __launch_bounds__(256) k_vanka_stencil_blk(Geo g, const cplx<TK>
                                                            const cplx<TK> *__restrict__ tab) {
   HMG_PDL_PROLOGUE();
   using S = BStencil<DIM, KIND>;
-  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
-  const int iyt = blockIdx.y * blockDim.y + threadIdx.y;
+  // 3D, launched with a one-dimensional block: FLAT (x, y) indexing -- consecutive threads run
+  // across the row ends, so rows of 2^k + 1 nodes leave no idle lanes (257 nodes: 9 warps of 32
+  // with the last one holding a single node; 129 nodes: 5 warps for 4.03 warps of work)
+  int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  int iyt = blockIdx.y * blockDim.y + threadIdx.y;
+  if (DIM == 3 && blockDim.y == 1) {
+    iyt = ix / g.n[0];
+    ix -= iyt * g.n[0];
+  }
   const int iy = DIM == 3 ? iyt : iyt * BZ;
   const int iz = DIM == 3 ? blockIdx.z * BZ : 0;
   if (ix >= g.n[0] || iy >= g.n[1] || iz >= g.n[2]) return;

@@ -317,6 +317,7 @@ template <typename T> struct Solver : SolverBase {
   bool stage3d = true;    // 3D fine operator: z-marching staged kernel (HMG_NO_STAGE3D=1 at build: the gather)
   bool fmarch = true;     // 2D c64 fine operator: warp-marching kernel (HMG_NO_FMARCH=1 at build: node-parallel)
   bool rbfast = true;     // RB sweep: constant-coefficient interior warps (HMG_NO_RB_FAST=1 at build: generic)
+  bool flat3d = true;     // register-blocked 3D stencils with flat (x, y) thread indexing (HMG_NO_FLAT3D=1 at build: off)
   int vanka_bz = 2;       // assembled-Vanka stencil: nodes per thread along the slow axis (HMG_VANKA_BZ at build)
   int smarch = 0;         // 2D c64 stored stencil: warp-marching kernel on large levels, segment height
                           // (HMG_SMARCH=8|16 at build; off by default: measured slower than the blocked gather)
@@ -402,6 +403,7 @@ template <typename T> struct Solver : SolverBase {
     // and hurts the 2D RB one (level 1 at N = 4096: 103 -> 117 ms)
     split_conc = std::getenv("HMG_NO_SPLIT_CONC") == nullptr;
     tile2d = std::getenv("HMG_NO_TILE2D") == nullptr;
+    flat3d = std::getenv("HMG_NO_FLAT3D") == nullptr;
     f32res = std::getenv("HMG_F64RES") == nullptr;
     vanka_bz = std::getenv("HMG_VANKA_BZ") ? std::atoi(std::getenv("HMG_VANKA_BZ")) : (opt.dim == 3 ? 2 : 1);
     if (comm && comm->size > 1) G = opt.intergrid == HMG_CUBIC ? 5 : 4;   // halo depth of the fused sweeps (u: 2 + r)
@@ -1454,16 +1456,21 @@ template <typename T> struct Solver : SolverBase {
         // one right-hand side on a large level: BZ = 4 planes per thread (register blocking)
         static const int bz_env = std::getenv("HMG_STORED_BZ") ? std::atoi(std::getenv("HMG_STORED_BZ")) : 4;
         const int bz = (NR == 1 && Lv.geo.n[2] >= 64) ? bz_env : 1;
-        dim3 grid4 = nl.grid;
+        dim3 grid4 = nl.grid, block4 = nl.block;
         grid4.z = (Lv.geo.n[2] + 3) / 4;
+        if (flat3d) {   // flat (x, y) indexing: no idle lanes on 2^k + 1-wide rows
+          block4 = dim3(256);
+          grid4.x = (unsigned)(((int64_t)Lv.geo.n[0] * Lv.geo.n[1] + 255) / 256);
+          grid4.y = 1;
+        }
         // radius 2, 4 planes per thread: capped at 64 registers for 4 blocks per SM (measured on
         // config 3 level 1: 46 -> 30 ms per solve on the same box; HMG_STORED_MINB=1: uncapped)
         static const int minb = std::getenv("HMG_STORED_MINB") ? std::atoi(std::getenv("HMG_STORED_MINB")) : 4;
         if (bz == 4 && minb >= 4 && Lv.r == 2) {
-          launch(k_stored_op<double, T, 3, 2, NR, 4, 4>, grid4, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv), ccl, ctb);
+          launch(k_stored_op<double, T, 3, 2, NR, 4, 4>, grid4, block4, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv), ccl, ctb);
         } else if (bz == 4) {
-          if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR, 4>, grid4, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<27, double>(uv), ccl, ctb);
-          else launch(k_stored_op<double, T, 3, 2, NR, 4>, grid4, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv), ccl, ctb);
+          if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR, 4>, grid4, block4, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<27, double>(uv), ccl, ctb);
+          else launch(k_stored_op<double, T, 3, 2, NR, 4>, grid4, block4, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv), ccl, ctb);
         } else {
           if (Lv.r == 1) launch(k_stored_op<double, T, 3, 1, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<27, double>(uv), ccl, ctb);
           else launch(k_stored_op<double, T, 3, 2, NR>, nl.grid, nl.block, 0, s, Lv.geo, cf, xq, fq, yq, bs, ub, ucopy<125, double>(uv), ccl, ctb);
@@ -1583,10 +1590,15 @@ template <typename T> struct Solver : SolverBase {
     if (nbat(l) == 1 && vbz > 1 && nslow >= 64) {
       tag(zero ? "vanka_zero" : "vanka", l, bop_bytes(l, NB) + (zero ? 2 : 3) * sizeof(TV) * nn);
       auto go = [&](auto kern, int bz) {
-        dim3 grid = nl.grid;
+        dim3 grid = nl.grid, block = nl.block;
         if (DIM == 3) grid.z = (Lv.geo.n[2] + bz - 1) / bz;
         else grid.y = (Lv.geo.n[1] + 8 * bz - 1) / (8 * bz);
-        launch(kern, grid, nl.block, 0, s, Lv.geo, (const C *)Lv.bop.template as<C>(), (const TV *)r, (const TV *)u,
+        if (DIM == 3 && flat3d) {   // flat (x, y) indexing: no idle lanes on 2^k + 1-wide rows
+          block = dim3(256);
+          grid.x = (unsigned)(((int64_t)Lv.geo.n[0] * Lv.geo.n[1] + 255) / 256);
+          grid.y = 1;
+        }
+        launch(kern, grid, block, 0, s, Lv.geo, (const C *)Lv.bop.template as<C>(), (const TV *)r, (const TV *)u,
                (TV *)u, (BV)damp(l), zero, Lv.ub, ucopy<NB, BV>(Lv.ubop), bop_cls(Lv), bop_tab(Lv));
       };
       if (vbz >= 4) go(k_vanka_stencil_blk<BV, T, DIM, KIND, 4>, 4);
@@ -2424,6 +2436,7 @@ template <typename T> struct Solver : SolverBase {
     c->zblock3 = zblock3;
     c->split_conc = split_conc;
     c->tile2d = tile2d;
+    c->flat3d = flat3d;
     c->f32res = f32res;
     c->tail_minb = tail_minb;
     c->usig = usig; c->uia = uia; c->uid = uid; c->usigd = usigd;
